@@ -1,0 +1,165 @@
+/*
+ * snapgpu.h -- C-ABI of the B200-native SNAP force engine.
+ *
+ * Drop-in boundary for the reference's stage interface (snapforge, header-only
+ * C++ under /root/reference/proj/include/snapforge).  The reference exposes
+ * no FFI; its boundary is the C++ stage signatures called by run_pipeline
+ * (pipeline.hpp:206-303).  Each entry point below names the reference
+ * function it replaces.  Conventions:
+ *
+ *   - extern "C", plain pointers and sizes, no exceptions across the ABI;
+ *   - every call returns an int status (SNAPGPU_OK == 0) and records a
+ *     message readable through snapgpu_last_error(ctx);
+ *   - a context is bound to one CUDA device and one stream, is not
+ *     thread-safe, and executes stream-ordered (like DescriptorState,
+ *     snap_core.hpp:130-172, it owns every per-atom array);
+ *   - pointers are HOST memory unless the name says "device";
+ *   - per-atom complex arrays returned by the debug getters are logical
+ *     (atom, half-index) order, interleaved re/im, half index space
+ *     2*mb <= t (halfint_index.hpp:16-25).
+ *
+ * Error codes mirror the reference exception types (common.hpp:21-42):
+ *   SNAPGPU_EINVAL    <- InvalidArgument (detail::require, Problem::validate)
+ *   SNAPGPU_EPIPELINE <- PipelineError
+ *   SNAPGPU_ECUDA     <- CUDA runtime failure (no reference analogue)
+ *   SNAPGPU_ESTATE    <- stage called before its inputs exist
+ */
+#ifndef SNAPGPU_H
+#define SNAPGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNAPGPU_OK 0
+#define SNAPGPU_EINVAL 1
+#define SNAPGPU_EPIPELINE 2
+#define SNAPGPU_ECUDA 3
+#define SNAPGPU_ESTATE 4
+
+#define SNAPGPU_MAX_TWOJMAX 14
+
+typedef struct snapgpu_ctx snapgpu_ctx;
+
+/* Message of the last failing call on ctx (or of the last failing
+ * context-free call when ctx is NULL).  Never NULL. */
+const char* snapgpu_last_error(const snapgpu_ctx* ctx);
+const char* snapgpu_version(void);
+
+/* ---- setup ------------------------------------------------------------
+ * Replaces SnapParams (snap_core.hpp:48-57) + HalfIntIndexMaps::build
+ * (halfint_index.hpp:155-200) + compute_cg_table (angular_basis.hpp:151-196)
+ * + the fold_beta table (snap_core.hpp:308-322, 1135-1138).  Builds every
+ * index/coefficient table on the host and uploads it once.
+ * twojmax in [0, SNAPGPU_MAX_TWOJMAX]; weights are per-type neighbor weights
+ * (SnapParams::weights); beta has n_triples(twojmax) entries.
+ */
+int snapgpu_create(int device, int twojmax, double rcut, double rmin0,
+                   double rfac0, double wself, int self_flag,
+                   const double* beta, int nbeta, const double* weights,
+                   int nweights, snapgpu_ctx** out);
+int snapgpu_destroy(snapgpu_ctx* ctx);
+
+/* Replace the linear model coefficients (SnapParams::beta) in place. */
+int snapgpu_set_beta(snapgpu_ctx* ctx, const double* beta, int nbeta);
+
+/* Run on a caller-owned CUDA stream (cudaStream_t passed as void*);
+ * NULL restores the context's own stream. */
+int snapgpu_set_stream(snapgpu_ctx* ctx, void* cuda_stream);
+
+/* ---- neighbor lists ---------------------------------------------------
+ * Replaces Problem::neighbors / Problem::types (snap_core.hpp:59-119) and
+ * performs Problem::validate (:89-118).  Flattened (atom, slot) arrays:
+ * nbr[i*stride+k], disp[(i*stride+k)*3+d] for k < numneigh[i]; types may be
+ * NULL (all type 0).  Host->device copies run on the context stream.
+ */
+int snapgpu_set_neighbors(snapgpu_ctx* ctx, int natoms, int stride,
+                          const int* numneigh, const int* nbr,
+                          const double* disp, const int* types);
+
+/* Atom-partitioned variant for multi-GPU runs: this context owns atoms
+ * [atom_lo, atom_lo+nlocal) of natoms_total; lists are given for the owned
+ * atoms only, with global neighbor indices; types (natoms_total) may be
+ * NULL.  Forces are produced as a natoms_total x 3 PARTIAL buffer (owned
+ * pairs' contributions to every atom) for a subsequent reduce-scatter. */
+int snapgpu_set_neighbors_partition(snapgpu_ctx* ctx, int natoms_total,
+                                    int atom_lo, int nlocal, int stride,
+                                    const int* numneigh, const int* nbr,
+                                    const double* disp, const int* types);
+
+/* ---- stages (snap_core.hpp), stream-ordered ---------------------------- */
+int snapgpu_compute_U(snapgpu_ctx* ctx);         /* compute_U        :369  */
+int snapgpu_compute_Y(snapgpu_ctx* ctx);         /* compute_Y        :1085,
+                                                    + per-atom energy
+                                                    (replaces compute_B_from_U
+                                                    :642 + compute_energy :684) */
+int snapgpu_compute_dU_deidrj(snapgpu_ctx* ctx); /* compute_fused_dE :1274
+                                                    (compute_dU :707 fused
+                                                    with compute_dE :1206)  */
+int snapgpu_scatter_forces(snapgpu_ctx* ctx);    /* scatter_forces   :872  */
+
+/* The whole force step in reference stage order (run_pipeline adjoint
+ * branch, pipeline.hpp:234-272): U -> Y(+energy) -> fused dU/dE -> scatter.
+ * Replayed from a CUDA graph after the first call for a given shape. */
+int snapgpu_run(snapgpu_ctx* ctx);
+int snapgpu_synchronize(snapgpu_ctx* ctx);
+
+/* ---- results (host copies; synchronize the stream) ---------------------
+ * forces: natoms_total x 3 (PipelineResult::forces, pipeline.hpp:50);
+ * eatom: nlocal (EnergyReport::per_atom); etotal: sum over owned atoms. */
+int snapgpu_get_forces(snapgpu_ctx* ctx, double* forces);
+int snapgpu_get_energy(snapgpu_ctx* ctx, double* eatom, double* etotal);
+
+/* Debug readback in the reference's logical conventions:
+ * ulisttot / ylist: nlocal x n_half complex (DescriptorState::ulisttot /
+ * ylist, snap_core.hpp:138-139); dedr: nlocal x stride x 3
+ * (DescriptorState::delist, :144). */
+int snapgpu_get_ulisttot(snapgpu_ctx* ctx, double* out);
+int snapgpu_get_ylist(snapgpu_ctx* ctx, double* out);
+int snapgpu_get_dedr(snapgpu_ctx* ctx, double* out);
+
+/* Device pointers for collectives (valid until the next set_neighbors):
+ * forces natoms_total x 3, eatom nlocal, etotal 1. */
+int snapgpu_device_outputs(snapgpu_ctx* ctx, double** forces, double** eatom,
+                           double** etotal);
+
+/* Per-stage device times (ms) of the last snapgpu_run when timing is on:
+ * out[0..3] = U, Y, dE, scatter. */
+int snapgpu_enable_stage_timing(snapgpu_ctx* ctx, int on);
+int snapgpu_stage_times(snapgpu_ctx* ctx, float* out4);
+
+/* Launch tuning knobs (for benchmarking sweeps); 0 = automatic. */
+int snapgpu_tune(snapgpu_ctx* ctx, int y_warps, int y_parts, int de_warps);
+
+/* ---- context-free host utilities --------------------------------------- */
+
+/* Table sizes for a band limit (HalfIntIndexMaps, halfint_index.hpp:85-98):
+ * out[0..5] = n_triples, n_tuples, u_full_total, u_half_total,
+ * z_total_elements, cg_total. */
+int snapgpu_counts(int twojmax, int* out6);
+
+/* Periodic orthorhombic neighbor lists (harness.hpp:119-202, generalized
+ * from cubic): strict r < rcut, minimum image, each list sorted by neighbor
+ * index, displacement from center to neighbor.  Returns the maximum
+ * neighbor count (>= 0) or a negative status.  When the maximum exceeds
+ * maxstride only numneigh is written. */
+int snapgpu_build_neighborlist(const double* positions, int n,
+                               const double box[3], double rcut,
+                               int maxstride, int* numneigh, int* nbr,
+                               double* disp);
+
+/* Seeded BCC lattice (TestSNAP tungsten workload; not in the reference):
+ * nx*ny*nz cells, edge a, z-major atom order ((cz*ny+cy)*nx+cx)*2+basis,
+ * beta ~ U(-1,1) drawn first from an mt19937_64 seeded with `seed`
+ * (rng.hpp:19-29, harness.hpp:208-213), then a uniform jitter in
+ * [-jitter, jitter) per coordinate.  Returns the atom count. */
+int snapgpu_bcc_lattice(int nx, int ny, int nz, double a, double jitter,
+                        uint64_t seed, int twojmax, double* positions,
+                        double* beta);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNAPGPU_H */

@@ -1,0 +1,389 @@
+"""B200-native SNAP force engine (TestSNAP workload of arXiv 2011.12875).
+
+Host-side mirror of the reference's stage interface (snapforge,
+/root/reference/proj/include/snapforge) over the C-ABI in include/snapgpu.h,
+implemented by hand-written sm_100a FP64 kernels in csrc/.
+
+    Problem            <- snapforge::Problem / SnapParams   (snap_core.hpp:48-119)
+    SnapEngine         <- DescriptorState + stage functions (snap_core.hpp:130-1406)
+      .compute_U()            compute_U            :369
+      .compute_Y()            compute_Y            :1085  (+ per-atom energy)
+      .compute_fused_dE()     compute_fused_dE     :1274  (compute_dU + compute_deidrj)
+      .scatter_forces()       scatter_forces       :872
+    run_pipeline()     <- run_pipeline (pipeline.hpp:206), adjoint `fused` branch
+    build_neighborlist <- harness::build_neighborlist (harness.hpp:119)
+    bcc_problem        TestSNAP BCC tungsten generator (new; not in the reference)
+
+There is no CPU fallback: if the CUDA extension is missing or no GPU is
+present, engine construction raises.  Errors map onto the reference's
+exception types (common.hpp:21-42): InvalidArgument, PipelineError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "InvalidArgument", "PipelineError", "CudaError", "StateError", "Problem",
+    "PipelineResult", "SnapEngine", "run_pipeline", "build_neighborlist", "bcc_problem",
+    "counts", "library", "LIB_PATH",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libsnapgpu.so")
+
+
+class InvalidArgument(ValueError):
+    """snapforge::InvalidArgument (common.hpp:21-25)."""
+
+
+class PipelineError(RuntimeError):
+    """snapforge::PipelineError (common.hpp:28-31)."""
+
+
+class CudaError(PipelineError):
+    """CUDA runtime failure inside the engine."""
+
+
+class StateError(PipelineError):
+    """A stage was called before its inputs exist."""
+
+
+_ERRS = {1: InvalidArgument, 2: PipelineError, 3: CudaError, 4: StateError}
+
+_lib = None
+
+
+def library() -> C.CDLL:
+    """Load libsnapgpu.so (built by __graft_entry__.build()); fail loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} missing: the CUDA extension is not built "
+            "(run `python -c 'import __graft_entry__ as g; g.build()'`). "
+            "There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    vp, ip, dp = C.c_void_p, C.c_int, C.c_double
+    L.snapgpu_last_error.restype = C.c_char_p
+    L.snapgpu_last_error.argtypes = [vp]
+    L.snapgpu_version.restype = C.c_char_p
+    L.snapgpu_create.argtypes = [ip, ip, dp, dp, dp, dp, ip, vp, ip, vp, ip, C.POINTER(vp)]
+    L.snapgpu_destroy.argtypes = [vp]
+    L.snapgpu_set_beta.argtypes = [vp, vp, ip]
+    L.snapgpu_set_stream.argtypes = [vp, vp]
+    L.snapgpu_set_neighbors.argtypes = [vp, ip, ip, vp, vp, vp, vp]
+    L.snapgpu_set_neighbors_partition.argtypes = [vp, ip, ip, ip, ip, vp, vp, vp, vp]
+    for f in ("compute_U", "compute_Y", "compute_dU_deidrj", "scatter_forces", "run",
+              "synchronize"):
+        getattr(L, "snapgpu_" + f).argtypes = [vp]
+    L.snapgpu_get_forces.argtypes = [vp, vp]
+    L.snapgpu_get_energy.argtypes = [vp, vp, vp]
+    L.snapgpu_get_ulisttot.argtypes = [vp, vp]
+    L.snapgpu_get_ylist.argtypes = [vp, vp]
+    L.snapgpu_get_dedr.argtypes = [vp, vp]
+    L.snapgpu_device_outputs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
+    L.snapgpu_enable_stage_timing.argtypes = [vp, ip]
+    L.snapgpu_stage_times.argtypes = [vp, vp]
+    L.snapgpu_tune.argtypes = [vp, ip, ip, ip]
+    L.snapgpu_counts.argtypes = [ip, vp]
+    L.snapgpu_build_neighborlist.argtypes = [vp, ip, vp, dp, ip, vp, vp, vp]
+    L.snapgpu_bcc_lattice.argtypes = [ip, ip, ip, dp, dp, C.c_uint64, ip, vp, vp]
+    _lib = L
+    return L
+
+
+def _check(rc: int, ctx=None) -> None:
+    if rc != 0:
+        L = library()
+        msg = L.snapgpu_last_error(ctx).decode()
+        raise _ERRS.get(rc, PipelineError)(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def counts(twojmax: int) -> dict:
+    """Index-map sizes (HalfIntIndexMaps, halfint_index.hpp:85-98)."""
+    out = np.zeros(6, np.int32)
+    _check(library().snapgpu_counts(int(twojmax), out.ctypes.data))
+    keys = ("n_triples", "n_tuples", "u_full_total", "u_half_total", "z_total_elements",
+            "cg_total")
+    return dict(zip(keys, (int(x) for x in out)))
+
+
+@dataclass
+class Problem:
+    """snapforge::Problem + SnapParams (snap_core.hpp:48-119), flattened.
+
+    numneigh[i] neighbors of atom i live in slots k < numneigh[i] of
+    nbr[i, k] (int32) and disp[i, k, :] (float64, center -> neighbor).
+    """
+
+    twojmax: int = 8
+    rcut: float = 4.7
+    rmin0: float = 0.0
+    rfac0: float = 0.99363
+    wself: float = 1.0
+    self_flag: int = 1
+    beta: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    weights: np.ndarray = field(default_factory=lambda: np.ones(1))
+    numneigh: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    nbr: np.ndarray = field(default_factory=lambda: np.zeros((0, 0), np.int32))
+    disp: np.ndarray = field(default_factory=lambda: np.zeros((0, 0, 3)))
+    types: Optional[np.ndarray] = None
+    positions: Optional[np.ndarray] = None
+    box: Optional[np.ndarray] = None
+
+    @property
+    def natoms(self) -> int:
+        return int(np.asarray(self.numneigh).shape[0])
+
+    @property
+    def stride(self) -> int:
+        nbr = np.asarray(self.nbr)
+        return int(nbr.shape[1]) if nbr.ndim == 2 else int(nbr.size // max(self.natoms, 1))
+
+    @property
+    def npairs(self) -> int:
+        return int(np.asarray(self.numneigh).sum())
+
+    @classmethod
+    def from_any(cls, p) -> "Problem":
+        if isinstance(p, cls):
+            return p
+        kw = {k: getattr(p, k) for k in ("twojmax", "rcut", "rmin0", "rfac0", "wself",
+                                          "self_flag", "beta", "numneigh", "nbr", "disp")}
+        for k in ("weights", "types", "positions", "box"):
+            if getattr(p, k, None) is not None:
+                kw[k] = getattr(p, k)
+        return cls(**kw)
+
+
+@dataclass
+class PipelineResult:
+    """The parts of snapforge::PipelineResult (pipeline.hpp:47-70) the GPU path fills."""
+
+    forces: np.ndarray
+    eatom: np.ndarray
+    etotal: float
+    stage_ms: Optional[dict] = None
+
+
+class SnapEngine:
+    """A device context: tables uploaded once, stages launched stream-ordered.
+
+    Mirrors the reference's DescriptorState + stage functions; the arrays
+    live in HBM and are read back only through the getters.
+    """
+
+    def __init__(self, twojmax=8, rcut=4.7, rmin0=0.0, rfac0=0.99363, wself=1.0,
+                 self_flag=1, beta=None, weights=(1.0,), device=0):
+        L = library()
+        self._L = L
+        self.twojmax = int(twojmax)
+        self._beta = np.ascontiguousarray(beta, np.float64)
+        self._weights = np.ascontiguousarray(weights, np.float64)
+        h = C.c_void_p()
+        _check(L.snapgpu_create(int(device), self.twojmax, float(rcut), float(rmin0),
+                                float(rfac0), float(wself), int(self_flag),
+                                self._beta.ctypes.data, int(self._beta.size),
+                                self._weights.ctypes.data, int(self._weights.size),
+                                C.byref(h)))
+        self._h = h
+        self.natoms_total = 0
+        self.nlocal = 0
+        self.stride = 0
+        self._keep = ()
+
+    @classmethod
+    def for_problem(cls, p, device=0) -> "SnapEngine":
+        p = Problem.from_any(p)
+        return cls(p.twojmax, p.rcut, p.rmin0, p.rfac0, p.wself, p.self_flag, p.beta,
+                   p.weights, device)
+
+    # -- lifetime ----------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.snapgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _c(self, rc):
+        _check(rc, self._h)
+
+    # -- inputs ------------------------------------------------------------
+    def set_stream(self, cuda_stream_handle: int | None):
+        self._c(self._L.snapgpu_set_stream(self._h, cuda_stream_handle))
+
+    def set_beta(self, beta):
+        b = np.ascontiguousarray(beta, np.float64)
+        self._c(self._L.snapgpu_set_beta(self._h, b.ctypes.data, int(b.size)))
+        self._beta = b
+
+    def set_neighbors(self, numneigh, nbr, disp, types=None):
+        nn = np.ascontiguousarray(numneigh, np.int32)
+        nb = np.ascontiguousarray(nbr, np.int32)
+        dp = np.ascontiguousarray(disp, np.float64)
+        ty = None if types is None else np.ascontiguousarray(types, np.int32)
+        n = int(nn.shape[0])
+        stride = int(nb.shape[1]) if nb.ndim == 2 else int(nb.size // max(n, 1))
+        self._c(self._L.snapgpu_set_neighbors(self._h, n, stride, nn.ctypes.data,
+                                              nb.ctypes.data, dp.ctypes.data, _ptr(ty)))
+        self.natoms_total, self.nlocal, self.stride = n, n, stride
+        self._keep = (nn, nb, dp, ty)
+
+    def set_problem(self, p):
+        p = Problem.from_any(p)
+        self.set_neighbors(p.numneigh, p.nbr, p.disp, p.types)
+
+    def set_neighbors_partition(self, natoms_total, atom_lo, numneigh, nbr, disp, types=None):
+        nn = np.ascontiguousarray(numneigh, np.int32)
+        nb = np.ascontiguousarray(nbr, np.int32)
+        dp = np.ascontiguousarray(disp, np.float64)
+        ty = None if types is None else np.ascontiguousarray(types, np.int32)
+        n = int(nn.shape[0])
+        stride = int(nb.shape[1]) if nb.ndim == 2 else int(nb.size // max(n, 1))
+        self._c(self._L.snapgpu_set_neighbors_partition(
+            self._h, int(natoms_total), int(atom_lo), n, stride, nn.ctypes.data,
+            nb.ctypes.data, dp.ctypes.data, _ptr(ty)))
+        self.natoms_total, self.nlocal, self.stride = int(natoms_total), n, stride
+        self._keep = (nn, nb, dp, ty)
+
+    # -- stages (snap_core.hpp) ---------------------------------------------
+    def compute_U(self):
+        self._c(self._L.snapgpu_compute_U(self._h))
+
+    def compute_Y(self):
+        self._c(self._L.snapgpu_compute_Y(self._h))
+
+    def compute_fused_dE(self):
+        self._c(self._L.snapgpu_compute_dU_deidrj(self._h))
+
+    compute_dU_deidrj = compute_fused_dE
+
+    def scatter_forces(self):
+        self._c(self._L.snapgpu_scatter_forces(self._h))
+
+    def run(self):
+        self._c(self._L.snapgpu_run(self._h))
+
+    def synchronize(self):
+        self._c(self._L.snapgpu_synchronize(self._h))
+
+    def tune(self, y_warps=0, y_parts=0, de_warps=0):
+        self._c(self._L.snapgpu_tune(self._h, int(y_warps), int(y_parts), int(de_warps)))
+
+    def enable_stage_timing(self, on=True):
+        self._c(self._L.snapgpu_enable_stage_timing(self._h, int(bool(on))))
+
+    def stage_times(self) -> dict:
+        out = np.zeros(4, np.float32)
+        self._c(self._L.snapgpu_stage_times(self._h, out.ctypes.data))
+        return dict(zip(("U", "Y", "dE", "forces"), (float(x) for x in out)))
+
+    # -- outputs -------------------------------------------------------------
+    def forces(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        f = out if out is not None else np.zeros((self.natoms_total, 3), np.float64)
+        self._c(self._L.snapgpu_get_forces(self._h, f.ctypes.data))
+        return f
+
+    def energy(self):
+        e = np.zeros(self.nlocal, np.float64)
+        t = np.zeros(1, np.float64)
+        self._c(self._L.snapgpu_get_energy(self._h, e.ctypes.data, t.ctypes.data))
+        return e, float(t[0])
+
+    def ulisttot(self) -> np.ndarray:
+        nh = counts(self.twojmax)["u_half_total"]
+        o = np.zeros((self.nlocal, nh, 2), np.float64)
+        self._c(self._L.snapgpu_get_ulisttot(self._h, o.ctypes.data))
+        return o.view(np.complex128)[..., 0]
+
+    def ylist(self) -> np.ndarray:
+        nh = counts(self.twojmax)["u_half_total"]
+        o = np.zeros((self.nlocal, nh, 2), np.float64)
+        self._c(self._L.snapgpu_get_ylist(self._h, o.ctypes.data))
+        return o.view(np.complex128)[..., 0]
+
+    def dedr(self) -> np.ndarray:
+        o = np.zeros((self.nlocal, self.stride, 3), np.float64)
+        self._c(self._L.snapgpu_get_dedr(self._h, o.ctypes.data))
+        return o
+
+    def device_outputs(self):
+        f, e, t = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self._c(self._L.snapgpu_device_outputs(self._h, C.byref(f), C.byref(e), C.byref(t)))
+        return f.value, e.value, t.value
+
+
+def run_pipeline(problem, device=0, stage_timing=False) -> PipelineResult:
+    """run_pipeline (pipeline.hpp:206-303) for the fused adjoint path on the GPU."""
+    p = Problem.from_any(problem)
+    with SnapEngine.for_problem(p, device) as eng:
+        eng.set_problem(p)
+        if stage_timing:
+            eng.enable_stage_timing(True)
+        eng.run()
+        f = eng.forces()
+        e, t = eng.energy()
+        st = eng.stage_times() if stage_timing else None
+    return PipelineResult(forces=f, eatom=e, etotal=t, stage_ms=st)
+
+
+def build_neighborlist(positions, box, rcut):
+    """harness::build_neighborlist (harness.hpp:119-202), orthorhombic boxes."""
+    L = library()
+    pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+    n = pos.shape[0]
+    bx = np.ascontiguousarray(np.broadcast_to(np.asarray(box, np.float64), (3,)))
+    numneigh = np.zeros(n, np.int32)
+    mx = L.snapgpu_build_neighborlist(pos.ctypes.data, n, bx.ctypes.data, float(rcut), 0,
+                                      numneigh.ctypes.data, None, None)
+    if mx < 0:
+        _check(-mx)
+    s = max(mx, 1)
+    nbr = np.zeros((n, s), np.int32)
+    disp = np.zeros((n, s, 3), np.float64)
+    mx = L.snapgpu_build_neighborlist(pos.ctypes.data, n, bx.ctypes.data, float(rcut), s,
+                                      numneigh.ctypes.data, nbr.ctypes.data, disp.ctypes.data)
+    if mx < 0:
+        _check(-mx)
+    return numneigh, nbr, disp
+
+
+def bcc_problem(nx, ny, nz, twojmax=8, seed=2011, a=3.1803, jitter=0.05, rcut=4.7) -> Problem:
+    """TestSNAP BCC tungsten: nx*ny*nz cells (2 atoms each), 26 neighbors per atom."""
+    L = library()
+    n = 2 * nx * ny * nz
+    pos = np.zeros((n, 3), np.float64)
+    beta = np.zeros(counts(twojmax)["n_triples"], np.float64)
+    rc = L.snapgpu_bcc_lattice(int(nx), int(ny), int(nz), float(a), float(jitter),
+                               int(seed), int(twojmax), pos.ctypes.data, beta.ctypes.data)
+    if rc < 0:
+        _check(-rc)
+    box = np.array([nx * a, ny * a, nz * a])
+    numneigh, nbr, disp = build_neighborlist(pos, box, rcut)
+    return Problem(twojmax=int(twojmax), rcut=float(rcut), beta=beta, numneigh=numneigh,
+                   nbr=nbr, disp=disp, positions=pos, box=box)

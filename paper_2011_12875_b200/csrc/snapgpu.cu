@@ -1,0 +1,855 @@
+// snapgpu.cu -- context, launches and the C-ABI (include/snapgpu.h).
+//
+// A context mirrors the reference's DescriptorState (snap_core.hpp:130-172):
+// it owns every per-atom array, here in HBM, plus the host-built tables
+// (tables.cpp).  Stage entry points launch the kernels of kernels.cuh on the
+// context stream; snapgpu_run replays the whole force step from a CUDA graph.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/snapgpu.h"
+#include "kernels.cuh"
+#include "tables.hpp"
+
+using namespace snapgpu;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+struct CudaError {
+  std::string msg;
+};
+
+#define CK(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw CudaError{std::string(#expr) + ": " + cudaGetErrorString(_e)};              \
+  } while (0)
+
+struct InvalidArg {
+  std::string msg;
+};
+struct StateErr {
+  std::string msg;
+};
+
+void require(bool ok, const std::string& m) {
+  if (!ok) throw InvalidArg{m};
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) return;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct snapgpu_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // parameters (SnapParams, snap_core.hpp:48-57)
+  int T = 0;
+  GeoParams gp{};
+  std::vector<double> beta, weights;
+  IndexMaps maps;
+  std::vector<double> cg, hf, ywgt;
+
+  // device tables
+  DevBuf<double> d_weights, d_W, d_cg, d_bfold, d_hf, d_ywgt;
+  DevBuf<int> d_expand, d_tasks, d_tuples, d_einfo, d_etups, d_halfoff;
+  int task_cap = 0;
+  int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;
+  int y_gen_ta = 32;
+
+  // problem shape
+  std::vector<int> h_numneigh;
+  int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
+  bool have_lists = false, have_U = false, have_Y = false, have_dE = false;
+
+  // device arrays
+  DevBuf<int> d_numneigh, d_nbr, d_types;
+  DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal;
+
+  // graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_valid = false;
+
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[5] = {};
+  float stage_ms[4] = {0, 0, 0, 0};
+};
+
+namespace {
+
+void invalidate_graph(snapgpu_ctx* c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  c->gexec = nullptr;
+  c->graph = nullptr;
+  c->graph_valid = false;
+}
+
+template <class F>
+int guarded(snapgpu_ctx* c, F&& f) {
+  try {
+    if (c) CK(cudaSetDevice(c->device));
+    f();
+    return SNAPGPU_OK;
+  } catch (const InvalidArg& e) {
+    (c ? c->err : g_err) = e.msg;
+    return SNAPGPU_EINVAL;
+  } catch (const StateErr& e) {
+    (c ? c->err : g_err) = e.msg;
+    return SNAPGPU_ESTATE;
+  } catch (const CudaError& e) {
+    (c ? c->err : g_err) = e.msg;
+    return SNAPGPU_ECUDA;
+  } catch (const std::exception& e) {
+    (c ? c->err : g_err) = e.what();
+    return SNAPGPU_EPIPELINE;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// constant-memory upload of the specialized C' tables (once per device, T)
+// ---------------------------------------------------------------------------
+void upload_cprime(int device, int T, const IndexMaps& m, const std::vector<double>& cg) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == device && d.second == T) return;
+  const std::vector<double> cp = cprime_table(m, cg);
+  CK(cudaMemcpyToSymbol(cCP, cp.data(), cp.size() * sizeof(double),
+                        static_cast<size_t>(cp_base(T)) * sizeof(double)));
+  done.push_back({device, T});
+}
+
+// ---------------------------------------------------------------------------
+// template dispatch over twojmax
+// ---------------------------------------------------------------------------
+template <template <int> class F, class... Args>
+void dispatch_T(int T, Args&&... args) {
+  switch (T) {
+    case 0: F<0>::go(args...); break;
+    case 1: F<1>::go(args...); break;
+    case 2: F<2>::go(args...); break;
+    case 3: F<3>::go(args...); break;
+    case 4: F<4>::go(args...); break;
+    case 5: F<5>::go(args...); break;
+    case 6: F<6>::go(args...); break;
+    case 7: F<7>::go(args...); break;
+    case 8: F<8>::go(args...); break;
+    case 9: F<9>::go(args...); break;
+    case 10: F<10>::go(args...); break;
+    case 11: F<11>::go(args...); break;
+    case 12: F<12>::go(args...); break;
+    case 13: F<13>::go(args...); break;
+    case 14: F<14>::go(args...); break;
+    default: throw InvalidArg{"twojmax outside [0, 14]"};
+  }
+}
+
+PairArgs pair_args(const snapgpu_ctx* c) {
+  PairArgs p;
+  p.nlocal = c->nlocal;
+  p.stride = c->stride;
+  p.atom_lo = c->atom_lo;
+  p.numneigh = c->d_numneigh.p;
+  p.nbr = c->d_nbr.p;
+  p.disp = c->d_disp.p;
+  p.types = c->d_types.p;
+  p.weights = c->d_weights.p;
+  return p;
+}
+
+template <int T>
+struct LaunchU {
+  static void go(snapgpu_ctx* c) {
+    using C = UCfg<T>;
+    UArgs a;
+    a.pr = pair_args(c);
+    a.gp = c->gp;
+    a.V = c->d_V.p;
+    const size_t smem = sizeof(double) * ((size_t)C::WARPS * c->stride * 5 +
+                                          (C::REGACC ? 0 : (size_t)C::WARPS * 2 * C::NACC * 32));
+    static bool attr = false;
+    if (!attr || smem > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_compute_U<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::max<size_t>(smem, 48 * 1024)));
+      attr = true;
+    }
+    const int blocks = (c->nlocal + C::WARPS - 1) / C::WARPS;
+    k_compute_U<T><<<blocks, C::WARPS * 32, smem, c->stream>>>(a);
+    CK(cudaGetLastError());
+  }
+};
+
+template <int T>
+struct LaunchY {
+  static void go(snapgpu_ctx* c) {
+    if constexpr (y_specialized(T)) {
+      constexpr int NF = c_full_off(T + 1);
+      YArgs a;
+      a.V = c->d_V.p;
+      a.Y = c->d_Y.p;
+      a.W = c->d_W.p;
+      a.expand = c->d_expand.p;
+      a.tasks = c->d_tasks.p;
+      a.task_cap = c->task_cap;
+      a.nlocal = c->nlocal;
+      a.eatom = c->d_eatom.p;
+      const size_t smem = sizeof(double) * 2 * NF * 32;
+      CK(cudaFuncSetAttribute(k_compute_Y_spec<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+      dim3 grid(c->ntiles, c->y_parts_used);
+      k_compute_Y_spec<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+      CK(cudaGetLastError());
+    } else {
+      YGArgs a;
+      a.V = c->d_V.p;
+      a.Y = c->d_Y.p;
+      a.cg = c->d_cg.p;
+      a.bfold = c->d_bfold.p;
+      a.tuples = c->d_tuples.p;
+      a.elem_info = c->d_einfo.p;
+      a.elem_tups = c->d_etups.p;
+      a.tasks = c->d_tasks.p;
+      a.task_cap = c->task_cap;
+      a.hf = c->d_hf.p;
+      a.ywgt = c->d_ywgt.p;
+      a.half_off = c->d_halfoff.p;
+      a.T = T;
+      a.NH = c->maps.nhalf;
+      a.nlocal = c->nlocal;
+      a.eatom = c->d_eatom.p;
+      const int TA = c->y_gen_ta;
+      const size_t smem = sizeof(double) * 2 * (size_t)a.NH * TA;
+      const int ncta = (c->ntiles * 32) / TA;
+      dim3 grid(ncta, c->y_parts_used);
+      if (TA == 32) {
+        CK(cudaFuncSetAttribute(k_compute_Y_gen<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        k_compute_Y_gen<32><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+      } else {
+        CK(cudaFuncSetAttribute(k_compute_Y_gen<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        k_compute_Y_gen<16><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+      }
+      CK(cudaGetLastError());
+    }
+  }
+};
+
+template <int T>
+struct LaunchDE {
+  static void go(snapgpu_ctx* c) {
+    using C = DECfg<T>;
+    DEArgs a;
+    a.pr = pair_args(c);
+    a.gp = c->gp;
+    a.Y = c->d_Y.p;
+    a.dedr = c->d_dedr.p;
+    a.nslots = c->nlocal * c->stride;
+    const int per_block = C::WARPS * C::PPW;
+    const int blocks = (a.nslots + per_block - 1) / per_block;
+    if (blocks > 0) {
+      k_fused_dE<T><<<blocks, C::WARPS * 32, 0, c->stream>>>(a);
+      CK(cudaGetLastError());
+    }
+  }
+};
+
+// Y work split: parts per tile so that small problems still fill the SMs.
+void plan_y(snapgpu_ctx* c) {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  const bool spec = y_specialized(c->T);
+  int units = spec ? c->ntiles : (c->ntiles * 32) / c->y_gen_ta;
+  int parts = c->y_parts;
+  if (parts <= 0) parts = std::max(1, std::min(8, nsm / std::max(1, units)));
+  c->y_parts_used = parts;
+  const int workers = parts * c->y_warps;
+  if (spec) {
+    std::vector<int> tasks = y_row_tasks(c->maps, workers, &c->task_cap);
+    c->d_tasks.alloc(tasks.size());
+    CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
+  } else {
+    GenericYPlan gpn = generic_y_plan(c->maps, workers);
+    c->task_cap = gpn.cap;
+    c->d_tasks.alloc(gpn.elem_tasks.size());
+    CK(cudaMemcpy(c->d_tasks.p, gpn.elem_tasks.data(), gpn.elem_tasks.size() * sizeof(int),
+                  cudaMemcpyHostToDevice));
+    c->d_einfo.alloc(gpn.elem_info.size());
+    CK(cudaMemcpy(c->d_einfo.p, gpn.elem_info.data(), gpn.elem_info.size() * sizeof(int),
+                  cudaMemcpyHostToDevice));
+    c->d_etups.alloc(std::max<size_t>(1, gpn.elem_tups.size()));
+    CK(cudaMemcpy(c->d_etups.p, gpn.elem_tups.data(), gpn.elem_tups.size() * sizeof(int),
+                  cudaMemcpyHostToDevice));
+  }
+}
+
+void upload_beta(snapgpu_ctx* c) {
+  const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data());
+  c->d_W.alloc(std::max<size_t>(1, W.size()));
+  CK(cudaMemcpy(c->d_W.p, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice));
+  std::vector<double> bf(c->maps.tuples.size());
+  for (size_t q = 0; q < bf.size(); ++q) {
+    const Tuple& tp = c->maps.tuples[q];
+    bf[q] = fold_beta(c->maps, c->beta.data(), tp.j1, tp.j2, tp.j);
+  }
+  c->d_bfold.alloc(std::max<size_t>(1, bf.size()));
+  CK(cudaMemcpy(c->d_bfold.p, bf.data(), bf.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+void launch_U(snapgpu_ctx* c) {
+  if (c->nlocal > 0) dispatch_T<LaunchU>(c->T, c);
+}
+void launch_Y(snapgpu_ctx* c) {
+  CK(cudaMemsetAsync(c->d_eatom.p, 0, sizeof(double) * std::max(1, c->nlocal), c->stream));
+  if (c->nlocal > 0) dispatch_T<LaunchY>(c->T, c);
+  k_energy_total<<<1, 1024, 0, c->stream>>>(c->d_eatom.p, c->nlocal, c->d_etotal.p);
+  CK(cudaGetLastError());
+}
+void launch_dE(snapgpu_ctx* c) {
+  if (c->nlocal > 0) dispatch_T<LaunchDE>(c->T, c);
+}
+void launch_scatter(snapgpu_ctx* c) {
+  CK(cudaMemsetAsync(c->d_forces.p, 0, sizeof(double) * 3 * std::max(1, c->natoms_total),
+                     c->stream));
+  ScatterArgs a;
+  a.pr = pair_args(c);
+  a.dedr = c->d_dedr.p;
+  a.forces = c->d_forces.p;
+  a.nslots = c->nlocal * c->stride;
+  if (a.nslots > 0) {
+    k_scatter_forces<<<(a.nslots + 255) / 256, 256, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw StateErr{std::string("stage called out of order: ") + what};
+}
+
+void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int stride,
+               const int* numneigh, const int* nbr, const double* disp, const int* types) {
+  require(natoms_total >= 0 && nlocal >= 0 && atom_lo >= 0 && atom_lo + nlocal <= natoms_total,
+          "problem: owned range outside the atom count");
+  require(nlocal == 0 || natoms_total > 0, "problem: no atoms");
+  require(stride >= 0, "problem: negative neighbor stride");
+  require(nlocal == 0 || stride == 0 || (numneigh && nbr && disp), "problem: null neighbor arrays");
+  const double rc2 = c->gp.rcut * c->gp.rcut;
+  const int nw = static_cast<int>(c->weights.size());
+  if (types)
+    for (int a = 0; a < natoms_total; ++a)
+      require(types[a] >= 0 && types[a] < nw, "problem: atom type outside weight table");
+  // Problem::validate (snap_core.hpp:89-118)
+  for (int i = 0; i < nlocal; ++i) {
+    require(numneigh[i] >= 0 && numneigh[i] <= stride, "problem: neighbor count outside stride");
+    for (int k = 0; k < numneigh[i]; ++k) {
+      const size_t pk = (size_t)i * stride + k;
+      const int j = nbr[pk];
+      require(j >= 0 && j < natoms_total, "problem: neighbor index out of range");
+      require(j != atom_lo + i, "problem: self neighbor");
+      const double* d = disp + pk * 3;
+      const double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+      require(r2 > 0.0, "problem: zero-length neighbor displacement");
+      require(r2 < rc2, "problem: neighbor at or beyond Rcut");
+    }
+  }
+  const bool reshape = natoms_total != c->natoms_total || nlocal != c->nlocal ||
+                       stride != c->stride || atom_lo != c->atom_lo ||
+                       (types != nullptr) != (c->d_types.p != nullptr);
+  if (reshape) invalidate_graph(c);
+  c->natoms_total = natoms_total;
+  c->atom_lo = atom_lo;
+  c->nlocal = nlocal;
+  c->stride = stride;
+  const int ntiles = (nlocal + 31) / 32;
+  const size_t nslots = (size_t)nlocal * stride;
+  const int NH = c->maps.nhalf;
+  const size_t vsz = (size_t)std::max(1, ntiles) * 2 * NH * 32;
+  if (reshape || ntiles != c->ntiles) {
+    c->d_numneigh.alloc(std::max(1, nlocal));
+    c->d_nbr.alloc(std::max<size_t>(1, nslots));
+    c->d_disp.alloc(std::max<size_t>(1, nslots * 3));
+    c->d_dedr.alloc(std::max<size_t>(1, nslots * 3));
+    c->d_forces.alloc((size_t)std::max(1, natoms_total) * 3);
+    c->d_eatom.alloc(std::max(1, nlocal));
+    c->d_etotal.alloc(1);
+    const bool grow = vsz > c->d_V.n;
+    c->d_V.alloc(vsz);
+    c->d_Y.alloc(vsz);
+    if (grow || ntiles != c->ntiles) {
+      CK(cudaMemsetAsync(c->d_V.p, 0, vsz * sizeof(double), c->stream));
+      CK(cudaMemsetAsync(c->d_Y.p, 0, vsz * sizeof(double), c->stream));
+    }
+    if (types) {
+      c->d_types.alloc(std::max(1, natoms_total));
+    } else {
+      c->d_types.release();
+    }
+    c->ntiles = ntiles;
+    plan_y(c);
+  }
+  if (nlocal > 0) {
+    CK(cudaMemcpyAsync(c->d_numneigh.p, numneigh, sizeof(int) * nlocal, cudaMemcpyHostToDevice,
+                       c->stream));
+    if (nslots > 0) {
+      CK(cudaMemcpyAsync(c->d_nbr.p, nbr, sizeof(int) * nslots, cudaMemcpyHostToDevice,
+                         c->stream));
+      CK(cudaMemcpyAsync(c->d_disp.p, disp, sizeof(double) * nslots * 3, cudaMemcpyHostToDevice,
+                         c->stream));
+    }
+  }
+  if (types)
+    CK(cudaMemcpyAsync(c->d_types.p, types, sizeof(int) * natoms_total, cudaMemcpyHostToDevice,
+                       c->stream));
+  c->h_numneigh.assign(numneigh, numneigh + nlocal);
+  c->have_lists = true;
+  c->have_U = c->have_Y = c->have_dE = false;
+}
+
+void record(snapgpu_ctx* c, int k) {
+  if (c->timing) CK(cudaEventRecord(c->ev[k], c->stream));
+}
+
+void run_direct(snapgpu_ctx* c) {
+  record(c, 0);
+  launch_U(c);
+  record(c, 1);
+  launch_Y(c);
+  record(c, 2);
+  launch_dE(c);
+  record(c, 3);
+  launch_scatter(c);
+  record(c, 4);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* snapgpu_last_error(const snapgpu_ctx* c) {
+  return c ? c->err.c_str() : g_err.c_str();
+}
+
+const char* snapgpu_version(void) { return "snapgpu 0.1 (sm_100a, FP64 SIMT, v-space)"; }
+
+int snapgpu_counts(int twojmax, int* out) {
+  return guarded(nullptr, [&] {
+    require(twojmax >= 0 && twojmax <= 64, "twojmax out of range");
+    require(out != nullptr, "null output");
+    IndexMaps m = IndexMaps::build(twojmax);
+    out[0] = static_cast<int>(m.triples.size());
+    out[1] = static_cast<int>(m.tuples.size());
+    out[2] = m.nfull;
+    out[3] = m.nhalf;
+    out[4] = m.zelems;
+    out[5] = m.cgtot;
+  });
+}
+
+int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rfac0,
+                   double wself, int self_flag, const double* beta, int nbeta,
+                   const double* weights, int nweights, snapgpu_ctx** out) {
+  snapgpu_ctx* c = nullptr;
+  const int rc = guarded(nullptr, [&] {
+    require(out != nullptr, "snapgpu_create: null output handle");
+    require(twojmax >= 0 && twojmax <= SNAPGPU_MAX_TWOJMAX,
+            "snapgpu_create: twojmax outside [0, 14]");
+    require(rcut > rmin0, "problem: Rcut must exceed rmin0");  // snap_core.hpp:98
+    require(nweights > 0 && weights, "problem: empty weight table");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    require(device >= 0 && device < ndev, "snapgpu_create: no such CUDA device");
+    CK(cudaSetDevice(device));
+    c = new snapgpu_ctx();
+    c->device = device;
+    c->T = twojmax;
+    c->maps = IndexMaps::build(twojmax);
+    require(nbeta == static_cast<int>(c->maps.triples.size()) && beta,
+            "problem: beta length must match the triple count");
+    c->gp.rcut = rcut;
+    c->gp.rmin0 = rmin0;
+    c->gp.rfac0 = rfac0;
+    c->gp.wself = wself;
+    c->gp.self_flag = self_flag ? 1 : 0;
+    c->beta.assign(beta, beta + nbeta);
+    c->weights.assign(weights, weights + nweights);
+    c->cg = cg_table(c->maps);
+    c->hf = half_f(c->maps);
+    c->ywgt = half_ywgt(c->maps);
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    auto up = [](auto& buf, const auto& v) {
+      using E = typename std::decay_t<decltype(v)>::value_type;
+      buf.alloc(std::max<size_t>(1, v.size()));
+      CK(cudaMemcpy(buf.p, v.data(), v.size() * sizeof(E), cudaMemcpyHostToDevice));
+    };
+    up(c->d_weights, c->weights);
+    up(c->d_cg, c->cg);
+    up(c->d_hf, c->hf);
+    up(c->d_ywgt, c->ywgt);
+    up(c->d_expand, full_expand_map(c->maps));
+    up(c->d_halfoff, c->maps.half_off);
+    std::vector<int> tup;
+    for (const Tuple& tp : c->maps.tuples) tup.insert(tup.end(), {tp.j1, tp.j2, tp.j, tp.elem_off, tp.cg_off});
+    up(c->d_tuples, tup);
+    upload_beta(c);
+    if (y_specialized(twojmax)) upload_cprime(device, twojmax, c->maps, c->cg);
+    c->y_gen_ta = (2.0 * c->maps.nhalf * 32 * 8 <= 200.0 * 1024) ? 32 : 16;
+    *out = c;
+  });
+  if (rc != SNAPGPU_OK && c) {
+    snapgpu_destroy(c);
+    if (out) *out = nullptr;
+  }
+  return rc;
+}
+
+int snapgpu_destroy(snapgpu_ctx* c) {
+  if (!c) return SNAPGPU_OK;
+  cudaSetDevice(c->device);
+  invalidate_graph(c);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  c->d_weights.release();
+  c->d_W.release();
+  c->d_cg.release();
+  c->d_bfold.release();
+  c->d_hf.release();
+  c->d_ywgt.release();
+  c->d_expand.release();
+  c->d_tasks.release();
+  c->d_tuples.release();
+  c->d_einfo.release();
+  c->d_etups.release();
+  c->d_halfoff.release();
+  c->d_numneigh.release();
+  c->d_nbr.release();
+  c->d_types.release();
+  c->d_disp.release();
+  c->d_V.release();
+  c->d_Y.release();
+  c->d_dedr.release();
+  c->d_forces.release();
+  c->d_eatom.release();
+  c->d_etotal.release();
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return SNAPGPU_OK;
+}
+
+int snapgpu_set_beta(snapgpu_ctx* c, const double* beta, int nbeta) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    require(beta && nbeta == static_cast<int>(c->maps.triples.size()),
+            "problem: beta length must match the triple count");
+    CK(cudaStreamSynchronize(c->stream));
+    c->beta.assign(beta, beta + nbeta);
+    upload_beta(c);
+    c->have_Y = c->have_dE = false;
+  });
+}
+
+int snapgpu_set_stream(snapgpu_ctx* c, void* s) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+  });
+}
+
+int snapgpu_set_neighbors(snapgpu_ctx* c, int natoms, int stride, const int* numneigh,
+                          const int* nbr, const double* disp, const int* types) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    set_lists(c, natoms, 0, natoms, stride, numneigh, nbr, disp, types);
+  });
+}
+
+int snapgpu_set_neighbors_partition(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal,
+                                    int stride, const int* numneigh, const int* nbr,
+                                    const double* disp, const int* types) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    set_lists(c, natoms_total, atom_lo, nlocal, stride, numneigh, nbr, disp, types);
+  });
+}
+
+int snapgpu_compute_U(snapgpu_ctx* c) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_lists, "compute_U needs neighbor lists");
+    launch_U(c);
+    c->have_U = true;
+    c->have_Y = c->have_dE = false;
+  });
+}
+
+int snapgpu_compute_Y(snapgpu_ctx* c) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_U, "compute_Y: no Ulisttot");  // snap_core.hpp:1089
+    launch_Y(c);
+    c->have_Y = true;
+  });
+}
+
+int snapgpu_compute_dU_deidrj(snapgpu_ctx* c) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_Y, "compute_fused_dE: requires Ylist");  // snap_core.hpp:1278
+    launch_dE(c);
+    c->have_dE = true;
+  });
+}
+
+int snapgpu_scatter_forces(snapgpu_ctx* c) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_dE, "scatter_forces: no dElist");  // snap_core.hpp:876
+    launch_scatter(c);
+  });
+}
+
+int snapgpu_run(snapgpu_ctx* c) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_lists, "run: no neighbor lists");
+    if (c->timing) {
+      run_direct(c);
+      CK(cudaEventSynchronize(c->ev[4]));
+      for (int s = 0; s < 4; ++s) CK(cudaEventElapsedTime(&c->stage_ms[s], c->ev[s], c->ev[s + 1]));
+    } else {
+      if (!c->graph_valid) {
+        invalidate_graph(c);
+        cudaStream_t user = c->stream;
+        c->stream = c->own_stream;  // capture on our own (non-legacy) stream
+        CK(cudaStreamSynchronize(user));
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          run_direct(c);
+        } catch (...) {
+          cudaGraph_t g;
+          cudaStreamEndCapture(c->stream, &g);
+          if (g) cudaGraphDestroy(g);
+          c->stream = user;
+          throw;
+        }
+        CK(cudaStreamEndCapture(c->stream, &c->graph));
+        CK(cudaGraphInstantiate(&c->gexec, c->graph, 0));
+        c->stream = user;
+        c->graph_valid = true;
+      }
+      CK(cudaGraphLaunch(c->gexec, c->stream));
+    }
+    c->have_U = c->have_Y = c->have_dE = true;
+  });
+}
+
+int snapgpu_synchronize(snapgpu_ctx* c) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int snapgpu_get_forces(snapgpu_ctx* c, double* f) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_dE, "get_forces before the force pass");
+    require(f != nullptr, "null output");
+    CK(cudaMemcpyAsync(f, c->d_forces.p, sizeof(double) * 3 * c->natoms_total,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int snapgpu_get_energy(snapgpu_ctx* c, double* eatom, double* etotal) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_Y, "get_energy before compute_Y");
+    if (eatom && c->nlocal > 0)
+      CK(cudaMemcpyAsync(eatom, c->d_eatom.p, sizeof(double) * c->nlocal, cudaMemcpyDeviceToHost,
+                         c->stream));
+    if (etotal)
+      CK(cudaMemcpyAsync(etotal, c->d_etotal.p, sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// Readback of V / Y' converted to the reference's logical u-space half arrays.
+static void read_tiles(snapgpu_ctx* c, const double* dev, std::vector<double>& host) {
+  const int NH = c->maps.nhalf;
+  host.resize((size_t)c->ntiles * 2 * NH * 32);
+  CK(cudaMemcpyAsync(host.data(), dev, host.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+int snapgpu_get_ulisttot(snapgpu_ctx* c, double* out) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_U, "get_ulisttot before compute_U");
+    std::vector<double> h;
+    read_tiles(c, c->d_V.p, h);
+    const int NH = c->maps.nhalf;
+    for (int a = 0; a < c->nlocal; ++a)
+      for (int e = 0; e < NH; ++e) {
+        const size_t base = (size_t)(a >> 5) * 2 * NH * 32 + (a & 31);
+        const double inv = 1.0 / c->hf[e];
+        out[((size_t)a * NH + e) * 2] = h[base + (size_t)e * 32] * inv;
+        out[((size_t)a * NH + e) * 2 + 1] = h[base + (size_t)(NH + e) * 32] * inv;
+      }
+  });
+}
+
+int snapgpu_get_ylist(snapgpu_ctx* c, double* out) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_Y, "get_ylist before compute_Y");
+    std::vector<double> h;
+    read_tiles(c, c->d_Y.p, h);
+    const IndexMaps& m = c->maps;
+    const int NH = m.nhalf;
+    for (int a = 0; a < c->nlocal; ++a) {
+      const size_t base = (size_t)(a >> 5) * 2 * NH * 32 + (a & 31);
+      double* o = out + (size_t)a * NH * 2;
+      for (int t = 0; t <= m.T; ++t)
+        for (int mb = 0; 2 * mb <= t; ++mb)
+          for (int ma = 0; ma <= t; ++ma) {
+            const int e = m.half_off[t] + mb * (t + 1) + ma;
+            if (c->ywgt[e] != 0.0) {
+              const double s = c->hf[e] / c->ywgt[e];
+              o[2 * e] = h[base + (size_t)e * 32] * s;
+              o[2 * e + 1] = h[base + (size_t)(NH + e) * 32] * s;
+            }
+          }
+      // middle-row elements ma > t/2 are never computed on the device; they
+      // follow from the index-reversal symmetry (halfint_index.hpp:22-25)
+      for (int t = 0; t <= m.T; t += 2) {
+        const int mb = t / 2;
+        for (int ma = t / 2 + 1; ma <= t; ++ma) {
+          const int e = m.half_off[t] + mb * (t + 1) + ma;
+          const int src = m.half_off[t] + mb * (t + 1) + (t - ma);
+          const double sg = ((ma + mb) & 1) ? -1.0 : 1.0;
+          o[2 * e] = sg * o[2 * src];
+          o[2 * e + 1] = -sg * o[2 * src + 1];
+        }
+      }
+    }
+  });
+}
+
+int snapgpu_get_dedr(snapgpu_ctx* c, double* out) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_dE, "get_dedr before the force pass");
+    const size_t n = (size_t)c->nlocal * c->stride * 3;
+    std::vector<double> h(n);
+    if (n) {
+      CK(cudaMemcpyAsync(h.data(), c->d_dedr.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    // zero the unused (padding) slots like the reference's zero-filled dElist
+    for (int i = 0; i < c->nlocal; ++i) {
+      const int nn = c->h_numneigh[i];
+      for (int k = 0; k < c->stride; ++k)
+        for (int d = 0; d < 3; ++d) {
+          const size_t s = ((size_t)i * c->stride + k) * 3 + d;
+          out[s] = k < nn ? h[s] : 0.0;
+        }
+    }
+  });
+}
+
+int snapgpu_device_outputs(snapgpu_ctx* c, double** forces, double** eatom, double** etotal) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    if (forces) *forces = c->d_forces.p;
+    if (eatom) *eatom = c->d_eatom.p;
+    if (etotal) *etotal = c->d_etotal.p;
+  });
+}
+
+int snapgpu_enable_stage_timing(snapgpu_ctx* c, int on) {
+  if (!c) return SNAPGPU_EINVAL;
+  c->timing = on != 0;
+  return SNAPGPU_OK;
+}
+
+int snapgpu_stage_times(snapgpu_ctx* c, float* out4) {
+  if (!c) return SNAPGPU_EINVAL;
+  for (int s = 0; s < 4; ++s) out4[s] = c->stage_ms[s];
+  return SNAPGPU_OK;
+}
+
+int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int de_warps) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    require(y_warps >= 0 && y_warps <= 16, "tune: y_warps in [0,16]");
+    if (y_warps > 0) c->y_warps = y_warps;
+    c->y_parts = y_parts;
+    c->de_warps = de_warps;
+    invalidate_graph(c);
+    if (c->have_lists) plan_y(c);
+  });
+}
+
+int snapgpu_build_neighborlist(const double* pos, int n, const double box[3], double rcut,
+                               int maxstride, int* numneigh, int* nbr, double* disp) {
+  int mx = -1;
+  const int rc = guarded(nullptr, [&] {
+    require(n >= 0 && (n == 0 || pos) && box, "build_neighborlist: null input");
+    std::string err;
+    mx = build_neighborlist(pos, n, box, rcut, maxstride, numneigh, nbr, disp, &err);
+    if (mx < 0) throw InvalidArg{err};
+  });
+  return rc == SNAPGPU_OK ? mx : -rc;
+}
+
+int snapgpu_bcc_lattice(int nx, int ny, int nz, double a, double jitter, uint64_t seed,
+                        int twojmax, double* pos, double* beta) {
+  int n = -1;
+  const int rc = guarded(nullptr, [&] {
+    require(nx > 0 && ny > 0 && nz > 0 && a > 0.0 && pos && beta, "bcc_lattice: bad arguments");
+    n = bcc_lattice(nx, ny, nz, a, jitter, seed, twojmax, pos, beta);
+  });
+  return rc == SNAPGPU_OK ? n : -rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,421 @@
+// tables.cpp -- host-side setup for the B200 SNAP engine (see tables.hpp).
+//
+// Reference citations are relative to /root/reference/proj/include/snapforge/.
+#include "tables.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <random>
+
+namespace snapgpu {
+
+namespace {
+int full_block(int t) { return (t + 1) * (t + 1); }
+int half_block(int t) { return (t / 2 + 1) * (t + 1); }
+}  // namespace
+
+// HalfIntIndexMaps::build (halfint_index.hpp:155-200); triples and tuples are
+// enumerated in the same lexicographic order (:132-141, :184-198).
+IndexMaps IndexMaps::build(int T) {
+  IndexMaps m;
+  m.T = T;
+  m.half_off.assign(T + 2, 0);
+  m.full_off.assign(T + 2, 0);
+  for (int t = 0; t <= T; ++t) {
+    m.full_off[t + 1] = m.full_off[t] + full_block(t);
+    m.half_off[t + 1] = m.half_off[t] + half_block(t);
+  }
+  m.nhalf = m.half_off[T + 1];
+  m.nfull = m.full_off[T + 1];
+  const int nd = (T + 1) * (T + 1) * (T + 1);
+  m.triple_flat.assign(nd, -1);
+  m.tuple_flat.assign(nd, -1);
+  m.cg_flat.assign(nd, -1);
+  int elem = 0, cgo = 0;
+  for (int j1 = 0; j1 <= T; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int j = j1 - j2; j <= std::min(j1 + j2, T); j += 2) {
+        if (j >= j1) {
+          m.triple_flat[m.dense(j1, j2, j)] = static_cast<int>(m.triples.size());
+          m.triples.push_back({j1, j2, j});
+        }
+        m.tuple_flat[m.dense(j1, j2, j)] = static_cast<int>(m.tuples.size());
+        m.cg_flat[m.dense(j1, j2, j)] = cgo;
+        m.tuples.push_back({j1, j2, j, elem, cgo});
+        elem += half_block(j);
+        cgo += (j1 + 1) * (j2 + 1);
+      }
+  m.zelems = elem;
+  m.cgtot = cgo;
+  return m;
+}
+
+double factorial(int n) {  // angular_basis.hpp:38-47
+  static const std::array<double, 65> table = [] {
+    std::array<double, 65> t{};
+    t[0] = 1.0;
+    for (int i = 1; i <= 64; ++i) t[i] = t[i - 1] * i;
+    return t;
+  }();
+  return table[n];
+}
+
+static double deltacg(int j1, int j2, int j) {  // angular_basis.hpp:66-70
+  const double sfaccg = factorial((j1 + j2 + j) / 2 + 1);
+  return std::sqrt(factorial((j1 + j2 - j) / 2) * factorial((j1 - j2 + j) / 2) *
+                   factorial((-j1 + j2 + j) / 2) / sfaccg);
+}
+
+// Racah closed form, identical arithmetic to compute_cg_table
+// (angular_basis.hpp:151-196) so the table is bitwise equal.
+std::vector<double> cg_table(const IndexMaps& m) {
+  std::vector<double> cg(m.cgtot, 0.0);
+  for (const Tuple& tp : m.tuples) {
+    const int j1 = tp.j1, j2 = tp.j2, j = tp.j;
+    int idx = tp.cg_off;
+    for (int m1 = 0; m1 <= j1; ++m1) {
+      const int aa2 = 2 * m1 - j1;
+      for (int m2 = 0; m2 <= j2; ++m2, ++idx) {
+        const int bb2 = 2 * m2 - j2;
+        const int mm = (aa2 + bb2 + j) / 2;
+        if (mm < 0 || mm > j) continue;
+        double sum = 0.0;
+        const int zlo = std::max(0, std::max(-(j - j2 + aa2) / 2, -(j - j1 - bb2) / 2));
+        const int zhi = std::min((j1 + j2 - j) / 2, std::min((j1 - aa2) / 2, (j2 + bb2) / 2));
+        for (int zz = zlo; zz <= zhi; ++zz) {
+          const double ifac = (zz % 2) ? -1.0 : 1.0;
+          sum += ifac / (factorial(zz) * factorial((j1 + j2 - j) / 2 - zz) *
+                         factorial((j1 - aa2) / 2 - zz) * factorial((j2 + bb2) / 2 - zz) *
+                         factorial((j - j2 + aa2) / 2 + zz) *
+                         factorial((j - j1 - bb2) / 2 + zz));
+        }
+        const int cc2 = 2 * mm - j;
+        const double norm =
+            std::sqrt(factorial((j1 + aa2) / 2) * factorial((j1 - aa2) / 2) *
+                      factorial((j2 + bb2) / 2) * factorial((j2 - bb2) / 2) *
+                      factorial((j + cc2) / 2) * factorial((j - cc2) / 2) * (j + 1));
+        cg[idx] = sum * deltacg(j1, j2, j) * norm;
+      }
+    }
+  }
+  return cg;
+}
+
+// fold_beta (snap_core.hpp:308-322).
+double fold_beta(const IndexMaps& m, const double* beta, int j1, int j2, int j) {
+  if (j >= j1) {
+    const double b = beta[m.triple_index(j1, j2, j)];
+    if (j1 == j) return (j2 == j) ? 3.0 * b : 2.0 * b;
+    return b;
+  }
+  if (j >= j2) {
+    const double b = beta[m.triple_index(j, j2, j1)];
+    const double ratio = static_cast<double>(j1 + 1) / static_cast<double>(j + 1);
+    return (j2 == j ? 2.0 * b : b) * ratio;
+  }
+  const double b = beta[m.triple_index(j2, j, j1)];
+  return b * static_cast<double>(j1 + 1) / static_cast<double>(j + 1);
+}
+
+double g_scale(int t, int mb) { return std::sqrt(factorial(t - mb)); }
+double h_scale(int t, int ma) { return 1.0 / std::sqrt(factorial(t - ma) * factorial(ma)); }
+double f_scale(int t, int mb, int ma) { return g_scale(t, mb) * h_scale(t, ma); }
+
+std::vector<double> cprime_table(const IndexMaps& m, const std::vector<double>& cg) {
+  std::vector<double> out(m.cgtot, 0.0);
+  for (const Tuple& tp : m.tuples) {
+    const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+    for (int ma1 = 0; ma1 <= tp.j1; ++ma1)
+      for (int ma2 = 0; ma2 <= tp.j2; ++ma2) {
+        const int ma = ma1 + ma2 - D;
+        const int idx = tp.cg_off + ma1 * (tp.j2 + 1) + ma2;
+        if (ma < 0 || ma > tp.j) continue;
+        out[idx] = cg[idx] / (h_scale(tp.j1, ma1) * h_scale(tp.j2, ma2) * h_scale(tp.j, ma));
+      }
+  }
+  return out;
+}
+
+std::vector<double> w_table(const IndexMaps& m, const std::vector<double>& cg,
+                            const double* beta) {
+  std::vector<double> out(m.cgtot, 0.0);
+  auto G = [](int t, int mm) { return g_scale(t, std::min(mm, t - mm)); };
+  for (const Tuple& tp : m.tuples) {
+    const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+    const double bf = fold_beta(m, beta, tp.j1, tp.j2, tp.j);
+    for (int mb1 = 0; mb1 <= tp.j1; ++mb1)
+      for (int mb2 = 0; mb2 <= tp.j2; ++mb2) {
+        const int mb = mb1 + mb2 - D;
+        const int idx = tp.cg_off + mb1 * (tp.j2 + 1) + mb2;
+        if (mb < 0 || 2 * mb > tp.j) continue;
+        out[idx] = bf * cg[idx] / (G(tp.j1, mb1) * G(tp.j2, mb2) * g_scale(tp.j, mb));
+      }
+  }
+  return out;
+}
+
+std::vector<double> half_f(const IndexMaps& m) {
+  std::vector<double> out(m.nhalf);
+  for (int t = 0; t <= m.T; ++t)
+    for (int mb = 0; 2 * mb <= t; ++mb)
+      for (int ma = 0; ma <= t; ++ma)
+        out[m.half_off[t] + mb * (t + 1) + ma] = f_scale(t, mb, ma);
+  return out;
+}
+
+std::vector<double> half_ywgt(const IndexMaps& m) {
+  std::vector<double> out(m.nhalf);
+  for (int t = 0; t <= m.T; ++t)
+    for (int mb = 0; 2 * mb <= t; ++mb)
+      for (int ma = 0; ma <= t; ++ma) {
+        double w = 1.0;
+        if (2 * mb == t) w = (2 * ma < t) ? 1.0 : (2 * ma == t ? 0.5 : 0.0);
+        out[m.half_off[t] + mb * (t + 1) + ma] = w;
+      }
+  return out;
+}
+
+std::vector<int> full_expand_map(const IndexMaps& m) {
+  std::vector<int> out(m.nfull);
+  for (int t = 0; t <= m.T; ++t)
+    for (int mb = 0; mb <= t; ++mb)
+      for (int ma = 0; ma <= t; ++ma) {
+        int code;
+        if (2 * mb <= t) {
+          code = (m.half_off[t] + mb * (t + 1) + ma) * 4;
+        } else {
+          const int src = m.half_off[t] + (t - mb) * (t + 1) + (t - ma);
+          const bool neg = ((ma + mb) & 1) != 0;
+          code = src * 4 + 2 + (neg ? 1 : 0);
+        }
+        out[m.full_off[t] + mb * (t + 1) + ma] = code;
+      }
+  return out;
+}
+
+// Cost of one target row (j, mb) of compute_Y in FP64 instructions per atom:
+// per contributing (tuple, mb1): 6 per complex MAC of the row body, 2 per
+// output of the row update, plus the row loads.
+static double y_row_cost(const IndexMaps& m, int j, int mb) {
+  double c = 0.0;
+  for (const Tuple& tp : m.tuples) {
+    if (tp.j != j) continue;
+    const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+    const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
+    if (hi < lo) continue;
+    int macs = 0;
+    for (int ma = 0; ma <= j; ++ma) {
+      const int alo = std::max(0, ma + D - tp.j2), ahi = std::min(tp.j1, ma + D);
+      macs += std::max(0, ahi - alo + 1);
+    }
+    c += (hi - lo + 1) * (6.0 * macs + 2.0 * (j + 1) + 2.0 * (tp.j1 + tp.j2 + 2));
+  }
+  return c;
+}
+
+static std::vector<std::vector<int>> lpt(const std::vector<std::pair<double, int>>& items,
+                                         int workers) {
+  std::vector<std::pair<double, int>> sorted = items;
+  std::stable_sort(sorted.begin(), sorted.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<std::vector<int>> out(workers);
+  using E = std::pair<double, int>;
+  std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+  for (int w = 0; w < workers; ++w) pq.push({0.0, w});
+  for (const auto& it : sorted) {
+    E e = pq.top();
+    pq.pop();
+    out[e.second].push_back(it.second);
+    pq.push({e.first + it.first, e.second});
+  }
+  return out;
+}
+
+std::vector<int> y_row_tasks(const IndexMaps& m, int workers, int* cap) {
+  std::vector<std::pair<double, int>> items;
+  for (int j = 0; j <= m.T; ++j)
+    for (int mb = 0; 2 * mb <= j; ++mb) items.push_back({y_row_cost(m, j, mb), j * 64 + mb});
+  auto buckets = lpt(items, workers);
+  int c = 0;
+  for (auto& b : buckets) c = std::max<int>(c, static_cast<int>(b.size()));
+  c += 1;
+  std::vector<int> out(static_cast<std::size_t>(workers) * c, -1);
+  for (int w = 0; w < workers; ++w)
+    for (std::size_t k = 0; k < buckets[w].size(); ++k) out[w * c + k] = buckets[w][k];
+  *cap = c;
+  return out;
+}
+
+GenericYPlan generic_y_plan(const IndexMaps& m, int workers) {
+  GenericYPlan p;
+  std::vector<std::pair<double, int>> items;
+  for (int j = 0; j <= m.T; ++j)
+    for (int mb = 0; 2 * mb <= j; ++mb)
+      for (int ma = 0; ma <= j; ++ma) {
+        if (2 * mb == j && 2 * ma > j) continue;  // never read: zero weight
+        const int id = static_cast<int>(p.elem_info.size() / 6);
+        const int begin = static_cast<int>(p.elem_tups.size());
+        double cost = 0.0;
+        for (std::size_t q = 0; q < m.tuples.size(); ++q) {
+          const Tuple& tp = m.tuples[q];
+          if (tp.j != j) continue;
+          const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+          const int nb = std::min(tp.j1, mb + D) - std::max(0, mb + D - tp.j2) + 1;
+          const int na = std::min(tp.j1, ma + D) - std::max(0, ma + D - tp.j2) + 1;
+          if (nb <= 0 || na <= 0) continue;
+          p.elem_tups.push_back(static_cast<int>(q));
+          cost += nb * (na * 10.0 + 8.0);
+        }
+        const int hidx = m.half_off[j] + mb * (j + 1) + ma;
+        p.elem_info.insert(p.elem_info.end(),
+                           {j, mb, ma, hidx, begin, static_cast<int>(p.elem_tups.size())});
+        items.push_back({cost, id});
+      }
+  auto buckets = lpt(items, workers);
+  int c = 0;
+  for (auto& b : buckets) c = std::max<int>(c, static_cast<int>(b.size()));
+  c += 1;
+  p.cap = c;
+  p.elem_tasks.assign(static_cast<std::size_t>(workers) * c, -1);
+  for (int w = 0; w < workers; ++w)
+    for (std::size_t k = 0; k < buckets[w].size(); ++k) p.elem_tasks[w * c + k] = buckets[w][k];
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// Neighbor lists: harness.hpp:119-202 arithmetic (wrap_coord :82-86,
+// min_image :88-90, strict r2 < rc2, lists sorted by index), generalized to
+// orthorhombic boxes.  Each atom scans the 27 surrounding cells of a cell
+// list; the minimum-image displacement is odd-symmetric and the lists are
+// sorted, so the result is bitwise identical to the reference's half-stencil
+// construction (checked in tests/test_tables.py).
+// ---------------------------------------------------------------------------
+namespace {
+double wrap_coord(double x, double box) {
+  double w = x - box * std::floor(x / box);
+  return w >= box ? w - box : w;
+}
+double min_image(double d, double box) { return d - box * std::nearbyint(d / box); }
+struct Nb {
+  int idx;
+  double d[3];
+};
+}  // namespace
+
+int build_neighborlist(const double* pos, int n, const double box[3], double rcut,
+                       int maxstride, int* numneigh, int* nbr, double* disp,
+                       std::string* err) {
+  for (int d = 0; d < 3; ++d) {
+    if (!(box[d] > 0.0) || !(rcut > 0.0)) {
+      *err = "build_neighborlist: box and Rcut must be positive";
+      return -1;
+    }
+    if (!(rcut <= 0.5 * box[d])) {
+      *err = "build_neighborlist: Rcut must not exceed box/2";
+      return -1;
+    }
+  }
+  std::vector<double> w(static_cast<std::size_t>(n) * 3);
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) w[i * 3 + c] = wrap_coord(pos[i * 3 + c], box[c]);
+  const double rc2 = rcut * rcut;
+  std::vector<std::vector<Nb>> lists(n);
+  int nc[3];
+  bool cells = true;
+  for (int d = 0; d < 3; ++d) {
+    nc[d] = static_cast<int>(std::floor(box[d] / rcut));
+    if (nc[d] < 3) cells = false;
+  }
+  auto try_pair = [&](int i, int k, std::vector<Nb>& out) {
+    Nb e;
+    for (int c = 0; c < 3; ++c) e.d[c] = min_image(w[k * 3 + c] - w[i * 3 + c], box[c]);
+    const double r2 = e.d[0] * e.d[0] + e.d[1] * e.d[1] + e.d[2] * e.d[2];
+    if (r2 < rc2) {
+      e.idx = k;
+      out.push_back(e);
+    }
+  };
+  if (!cells) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < n; ++k)
+        if (k != i) try_pair(i, k, lists[i]);
+  } else {
+    const long ncell = static_cast<long>(nc[0]) * nc[1] * nc[2];
+    std::vector<int> cell_of(n);
+    std::vector<int> head(ncell + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      int ci[3];
+      for (int d = 0; d < 3; ++d) {
+        int idx = static_cast<int>(w[i * 3 + d] * (static_cast<double>(nc[d]) / box[d]));
+        ci[d] = idx >= nc[d] ? nc[d] - 1 : idx;
+      }
+      cell_of[i] = (ci[2] * nc[1] + ci[1]) * nc[0] + ci[0];
+      head[cell_of[i] + 1]++;
+    }
+    for (long c = 0; c < ncell; ++c) head[c + 1] += head[c];
+    std::vector<int> members(n), fill(head.begin(), head.end() - 1);
+    for (int i = 0; i < n; ++i) members[fill[cell_of[i]]++] = i;
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int i = 0; i < n; ++i) {
+      const int c = cell_of[i];
+      const int cx = c % nc[0], cy = (c / nc[0]) % nc[1], cz = c / (nc[0] * nc[1]);
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int ox = (cx + dx + nc[0]) % nc[0], oy = (cy + dy + nc[1]) % nc[1],
+                      oz = (cz + dz + nc[2]) % nc[2];
+            const long oc = (static_cast<long>(oz) * nc[1] + oy) * nc[0] + ox;
+            for (int s = head[oc]; s < head[oc + 1]; ++s) {
+              const int k = members[s];
+              if (k != i) try_pair(i, k, lists[i]);
+            }
+          }
+    }
+  }
+  int mx = 0;
+  for (int i = 0; i < n; ++i) {
+    std::sort(lists[i].begin(), lists[i].end(),
+              [](const Nb& a, const Nb& b) { return a.idx < b.idx; });
+    mx = std::max<int>(mx, static_cast<int>(lists[i].size()));
+  }
+  for (int i = 0; i < n; ++i) {
+    if (numneigh) numneigh[i] = static_cast<int>(lists[i].size());
+    if (mx > maxstride || !nbr || !disp) continue;
+    for (std::size_t k = 0; k < lists[i].size(); ++k) {
+      const std::size_t pk = static_cast<std::size_t>(i) * maxstride + k;
+      nbr[pk] = lists[i][k].idx;
+      for (int c = 0; c < 3; ++c) disp[pk * 3 + c] = lists[i][k].d[c];
+    }
+  }
+  return mx;
+}
+
+// BCC tungsten lattice.  The reference has no lattice builder; the draws use
+// its Rng mappings (rng.hpp:19-29) over std::mt19937_64 and its beta
+// convention (harness.hpp:208-213: beta first).
+int bcc_lattice(int nx, int ny, int nz, double a, double jitter, std::uint64_t seed,
+                int T, double* pos, double* beta) {
+  std::mt19937_64 eng(seed);
+  auto uni = [&](double lo, double hi) {
+    return lo + (hi - lo) * (static_cast<double>(eng() >> 11) * 0x1.0p-53);
+  };
+  const IndexMaps m = IndexMaps::build(T);
+  for (std::size_t l = 0; l < m.triples.size(); ++l) beta[l] = uni(-1.0, 1.0);
+  int n = 0;
+  for (int cz = 0; cz < nz; ++cz)
+    for (int cy = 0; cy < ny; ++cy)
+      for (int cx = 0; cx < nx; ++cx)
+        for (int b = 0; b < 2; ++b) {
+          const double h = 0.5 * b;
+          const double base[3] = {(cx + h) * a, (cy + h) * a, (cz + h) * a};
+          for (int d = 0; d < 3; ++d) pos[n * 3 + d] = base[d] + uni(-jitter, jitter);
+          ++n;
+        }
+  return n;
+}
+
+}  // namespace snapgpu

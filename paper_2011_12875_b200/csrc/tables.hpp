@@ -1,0 +1,97 @@
+// tables.hpp -- host-side setup for the B200 SNAP engine.
+//
+// Everything here runs once per context (or once per neighbor-list upload)
+// on the host: the integer index bookkeeping of the reference
+// (halfint_index.hpp), the Clebsch-Gordan table (angular_basis.hpp:151-196),
+// the beta multiplicity fold (snap_core.hpp:308-322), and the tables that
+// are specific to this engine's "v-space" formulation:
+//
+//   v(t,mb,ma) = f(t,mb,ma) u(t,mb,ma),  f = g(t,mb) h(t,ma),
+//   g(t,mb) = sqrt((t-mb)!),  h(t,ma) = 1/sqrt((t-ma)! ma!),
+//
+// under which the Wigner level recursion (angular_basis.hpp:232-257) loses
+// its sqrt(p/q) weights:  v(t,mb,ma) = conj(a) v(t-1,mb,ma)
+//                                       - conj(b) v(t-1,mb,ma-1).
+// The per-element scale factors are folded into the coupling tables (C')
+// and the beta-weighted row tables (W) consumed by the compute_Y kernel.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace snapgpu {
+
+struct Tuple {
+  int j1, j2, j, elem_off, cg_off;
+};
+
+// HalfIntIndexMaps (halfint_index.hpp:64-128), same enumeration order.
+struct IndexMaps {
+  int T = 0;
+  int nhalf = 0, nfull = 0, cgtot = 0, zelems = 0;
+  std::vector<int> half_off, full_off;           // T+2 entries
+  std::vector<std::array<int, 3>> triples;       // canonical (j1, j2, j)
+  std::vector<Tuple> tuples;                     // all coupling tuples
+  std::vector<int> triple_flat, tuple_flat, cg_flat;  // dense (T+1)^3 lookups
+
+  static IndexMaps build(int T);
+  int dense(int a, int b, int c) const { return (a * (T + 1) + b) * (T + 1) + c; }
+  int triple_index(int a, int b, int c) const { return triple_flat[dense(a, b, c)]; }
+};
+
+double factorial(int n);
+std::vector<double> cg_table(const IndexMaps& m);  // angular_basis.hpp:151-196
+double fold_beta(const IndexMaps& m, const double* beta, int j1, int j2, int j);
+
+// v-space scale factors.
+double g_scale(int t, int mb);   // sqrt((t-mb)!)
+double h_scale(int t, int ma);   // 1/sqrt((t-ma)! ma!)
+double f_scale(int t, int mb, int ma);  // g*h
+
+// C'(tuple; ma1, ma2) = cg / (h(j1,ma1) h(j2,ma2) h(j, ma1+ma2-D)); same layout
+// as the CG table (cg_offset + ma1*(j2+1) + ma2).
+std::vector<double> cprime_table(const IndexMaps& m, const std::vector<double>& cg);
+// W(tuple; mb1, mb2) = fold_beta * cg / (G(j1,mb1) G(j2,mb2) g(j, mb)),
+// G(t,m) = g(t, min(m, t-m)); zero where the target row is not stored.
+std::vector<double> w_table(const IndexMaps& m, const std::vector<double>& cg,
+                            const double* beta);
+
+// Per-half-index scale 1/f (u = v/f) and f, in half index order.
+std::vector<double> half_f(const IndexMaps& m);
+// Weight of a stored Y' element: 1 on strict rows, on the middle row of even
+// levels 1 (ma < t/2), 0.5 (ma == t/2), 0 (ma > t/2).
+std::vector<double> half_ywgt(const IndexMaps& m);
+
+// Full-index expansion map for the Y kernel: for full index (t,mb,ma),
+// src half index and sign (+1, or -1 with conj when mirrored).  Encoded
+// as src*4 + (mirrored?2:0) + (negative?1:0).
+std::vector<int> full_expand_map(const IndexMaps& m);
+
+// compute_Y work decomposition: target rows (j, mb), with a cost model
+// (complex MACs weighted by instruction counts), assigned to `workers`
+// buckets by longest-processing-time.  Returns per-worker lists packed as
+// [worker][k] = j*64 + mb, terminated by -1, each worker padded to `cap`.
+std::vector<int> y_row_tasks(const IndexMaps& m, int workers, int* cap);
+
+// Generic compute_Y (any T): Y target elements (j, mb, ma) with the tuples
+// feeding them; packed int records consumed by the generic kernel.
+struct GenericYPlan {
+  std::vector<int> elem_tasks;  // per worker lists of target element ids, -1 terminated
+  int cap = 0;
+  std::vector<int> elem_info;   // per target element: j, mb, ma, hidx, tup_begin, tup_end
+  std::vector<int> elem_tups;   // tuple ids
+};
+GenericYPlan generic_y_plan(const IndexMaps& m, int workers);
+
+// Reference-order neighbor list builder (harness.hpp:119-202, orthorhombic).
+// Returns max neighbor count or -1 (err set).
+int build_neighborlist(const double* pos, int n, const double box[3], double rcut,
+                       int maxstride, int* numneigh, int* nbr, double* disp,
+                       std::string* err);
+
+int bcc_lattice(int nx, int ny, int nz, double a, double jitter, std::uint64_t seed,
+                int T, double* pos, double* beta);
+
+}  // namespace snapgpu

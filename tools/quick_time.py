@@ -1,0 +1,38 @@
+"""Quick device timing of the force step (development helper)."""
+import sys, time
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+import paper_2011_12875_b200 as snap
+
+def run(nx, ny, nz, T=8, reps=10, tune=None):
+    p = snap.bcc_problem(nx, ny, nz, twojmax=T)
+    eng = snap.SnapEngine.for_problem(p)
+    eng.set_problem(p)
+    if tune: eng.tune(*tune)
+    eng.enable_stage_timing(True)
+    for _ in range(3): eng.run()
+    st = {k: [] for k in ("U", "Y", "dE", "forces")}
+    for _ in range(reps):
+        eng.run()
+        for k, v in eng.stage_times().items(): st[k].append(v)
+    med = {k: float(np.median(v)) for k, v in st.items()}
+    eng.enable_stage_timing(False)
+    eng.run(); eng.synchronize()
+    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps): eng.run()
+    eng.synchronize()
+    dt = (time.perf_counter() - t0) / reps * 1e3
+    n = p.natoms
+    print(f"T={T} N={n} tune={tune} stages(ms)={ {k: round(v,4) for k,v in med.items()} } graph step {dt:.4f} ms -> {n/dt:.1f} Katom-steps/s, {dt*1e3/n*1e3:.2f} ns/atom", flush=True)
+    eng.close()
+
+if __name__ == "__main__":
+    run(10, 10, 10)
+    run(64, 64, 32, reps=5)
+    for tn in [(4,1,0),(8,1,0),(12,1,0),(16,1,0)]:
+        run(64, 64, 32, reps=3, tune=tn)
+    run(10,10,10, tune=(8,1,0)); run(10,10,10, tune=(8,2,0)); run(10,10,10, tune=(16,1,0))
+    run(32, 32, 16, T=14, reps=2)
