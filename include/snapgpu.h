@@ -125,13 +125,22 @@ int snapgpu_get_dedr(snapgpu_ctx* ctx, double* out);
 int snapgpu_device_outputs(snapgpu_ctx* ctx, double** forces, double** eatom,
                            double** etotal);
 
+/* Stream-ordered device-to-device copy of the natoms_total x 3 force buffer
+ * into caller memory (e.g. a torch tensor feeding an NCCL reduce-scatter). */
+int snapgpu_get_forces_device(snapgpu_ctx* ctx, double* dst_device);
+/* Same for the owned atoms' total energy (1 double); eatom_dst (nlocal) may
+ * be NULL. */
+int snapgpu_get_energy_device(snapgpu_ctx* ctx, double* eatom_dst,
+                              double* etotal_dst);
+
 /* Per-stage device times (ms) of the last snapgpu_run when timing is on:
  * out[0..3] = U, Y, dE, scatter. */
 int snapgpu_enable_stage_timing(snapgpu_ctx* ctx, int on);
 int snapgpu_stage_times(snapgpu_ctx* ctx, float* out4);
 
-/* Launch tuning knobs (for benchmarking sweeps); 0 = automatic. */
-int snapgpu_tune(snapgpu_ctx* ctx, int y_warps, int y_parts, int de_warps);
+/* compute_Y launch knobs (benchmark sweeps); 0 = automatic: warps per CTA
+ * (<= 8), row-list parts per tile, atoms per CTA tile (8, 16 or 32). */
+int snapgpu_tune(snapgpu_ctx* ctx, int y_warps, int y_parts, int y_tile_atoms);
 
 /* ---- context-free host utilities --------------------------------------- */
 
@@ -149,6 +158,10 @@ int snapgpu_build_neighborlist(const double* positions, int n,
                                const double box[3], double rcut,
                                int maxstride, int* numneigh, int* nbr,
                                double* disp);
+
+/* Diagnostic: FP64 DFMA throughput probe on `device` (all SMs, independent
+ * DFMA chains).  tflops receives the measured FP64 rate, ms the duration. */
+int snapgpu_fp64_peak(int device, int iters, double* tflops, double* ms);
 
 /* Seeded BCC lattice (TestSNAP tungsten workload; not in the reference):
  * nx*ny*nz cells, edge a, z-major atom order ((cz*ny+cy)*nx+cx)*2+basis,

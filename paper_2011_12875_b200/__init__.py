@@ -88,6 +88,9 @@ def library() -> C.CDLL:
     L.snapgpu_get_ylist.argtypes = [vp, vp]
     L.snapgpu_get_dedr.argtypes = [vp, vp]
     L.snapgpu_device_outputs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
+    L.snapgpu_get_forces_device.argtypes = [vp, vp]
+    L.snapgpu_get_energy_device.argtypes = [vp, vp, vp]
+    L.snapgpu_fp64_peak.argtypes = [ip, ip, vp, vp]
     L.snapgpu_enable_stage_timing.argtypes = [vp, ip]
     L.snapgpu_stage_times.argtypes = [vp, vp]
     L.snapgpu_tune.argtypes = [vp, ip, ip, ip]
@@ -235,6 +238,12 @@ class SnapEngine:
 
     # -- inputs ------------------------------------------------------------
     def set_stream(self, cuda_stream_handle: int | None):
+        """Run on a caller stream (e.g. torch.cuda.current_stream().cuda_stream).
+
+        Handle 0 is CUDA's legacy default stream, which the C-ABI spells
+        cudaStreamLegacy (0x1); None restores the engine's own stream."""
+        if cuda_stream_handle == 0:
+            cuda_stream_handle = 1  # cudaStreamLegacy
         self._c(self._L.snapgpu_set_stream(self._h, cuda_stream_handle))
 
     def set_beta(self, beta):
@@ -292,8 +301,9 @@ class SnapEngine:
     def synchronize(self):
         self._c(self._L.snapgpu_synchronize(self._h))
 
-    def tune(self, y_warps=0, y_parts=0, de_warps=0):
-        self._c(self._L.snapgpu_tune(self._h, int(y_warps), int(y_parts), int(de_warps)))
+    def tune(self, y_warps=0, y_parts=0, y_tile_atoms=0):
+        """compute_Y launch knobs (0 = automatic)."""
+        self._c(self._L.snapgpu_tune(self._h, int(y_warps), int(y_parts), int(y_tile_atoms)))
 
     def enable_stage_timing(self, on=True):
         self._c(self._L.snapgpu_enable_stage_timing(self._h, int(bool(on))))
@@ -332,6 +342,14 @@ class SnapEngine:
         self._c(self._L.snapgpu_get_dedr(self._h, o.ctypes.data))
         return o
 
+    def forces_to_device(self, dst_ptr: int):
+        """Stream-ordered D2D copy of the force buffer into device memory dst_ptr."""
+        self._c(self._L.snapgpu_get_forces_device(self._h, dst_ptr))
+
+    def energy_to_device(self, etotal_ptr: int, eatom_ptr: int | None = None):
+        """Stream-ordered D2D copy of the owned total energy (and per-atom energies)."""
+        self._c(self._L.snapgpu_get_energy_device(self._h, eatom_ptr, etotal_ptr))
+
     def device_outputs(self):
         f, e, t = C.c_void_p(), C.c_void_p(), C.c_void_p()
         self._c(self._L.snapgpu_device_outputs(self._h, C.byref(f), C.byref(e), C.byref(t)))
@@ -350,6 +368,14 @@ def run_pipeline(problem, device=0, stage_timing=False) -> PipelineResult:
         e, t = eng.energy()
         st = eng.stage_times() if stage_timing else None
     return PipelineResult(forces=f, eatom=e, etotal=t, stage_ms=st)
+
+
+def fp64_peak(device=0, iters=200000):
+    """Measured FP64 DFMA throughput (TFLOP/s) of `device` (diagnostic probe)."""
+    t = np.zeros(1)
+    ms = np.zeros(1)
+    _check(library().snapgpu_fp64_peak(int(device), int(iters), t.ctypes.data, ms.ctypes.data))
+    return float(t[0]), float(ms[0])
 
 
 def build_neighborlist(positions, box, rcut):

@@ -3,8 +3,8 @@
 // Stage map (reference: /root/reference/proj/include/snapforge/snap_core.hpp):
 //   k_compute_U        compute_U            :369-489   (fused with the 3-sphere
 //                                                        map + switching function)
-//   k_compute_Y_spec   compute_Y            :1085-1200  (twojmax in {2,4,6,8};
-//   k_compute_Y_gen                                      generic for any twojmax)
+//   k_compute_Y        compute_Y            :1085-1200  (sliding-window CG
+//                                                        contraction, any twojmax)
 //                      + per-atom energy (replaces compute_B_from_U :642 and
 //                        compute_energy :684 through E_i = 1/3 sum Y:U*)
 //   k_fused_dE         compute_fused_dE     :1274-1406 (dU never reaches HBM)
@@ -70,18 +70,6 @@ __host__ __device__ constexpr int c_acc_off(int t) {  // sum_{s<t} (s/2+1)
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 
-// The specialized compute_Y kernels keep their C' coefficient tables in
-// constant memory (DFMA takes a constant-bank operand for free).
-__host__ __device__ constexpr bool y_specialized(int T) {
-  return T == 2 || T == 4 || T == 6 || T == 8;
-}
-__host__ __device__ constexpr int cp_base(int T) {
-  int o = 0;
-  for (int s = 2; s < T; s += 2) o += c_cg_total(s);
-  return o;
-}
-constexpr int kCpTotal = c_cg_total(2) + c_cg_total(4) + c_cg_total(6) + c_cg_total(8);
-__constant__ double cCP[kCpTotal];
 
 // ---------------------------------------------------------------------------
 // kernel argument blocks
@@ -372,121 +360,462 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32)
   }
 }
 
-// ===========================================================================
-// compute_Y, specialized (snap_core.hpp:1085-1200)
-//
-// CTA = one AoSoA tile of 32 atoms (lane = atom, so every lane runs the same
-// loop bounds and reads the same coefficient) x one "part" of the target
-// rows.  The tile's V is expanded once into shared memory as the full
-// mirrored stack X (split planes [re|im][full idx][32]: conflict-free LDS).
-// Each warp owns whole target rows (j, mb) and accumulates the row's j+1
-// outputs in registers across every coupling tuple (j1, j2) -> j and every
-// contributing row pair (mb1, mb2): per row pair it loads X row mb1 of level
-// j1 and row mb2 of level j2 into registers and runs the fully unrolled
-// (ma1, ma2) product body with C' coefficients from constant memory, so each
-// loaded complex feeds ~2 complex MACs.  Output: Y' (v-space, weighted).
-// Epilogue: per-atom energy E_i = 2/3 sum_{stored} Re(Y'_s conj V).
-// ===========================================================================
-struct YArgs {
-  const double* V;      // [tile][2][NH][32]
-  double* Y;            // [tile][2][NH][32]
-  const double* W;      // W table (cg layout)
-  const int* expand;    // full idx -> src code
-  const int* tasks;     // [worker][cap]
-  int task_cap;
-  int nlocal;
-  double* eatom;        // nlocal (accumulated with atomics)
+// ---------------------------------------------------------------------------
+// Energy epilogue shared by the compute_Y kernels: per-atom energies are
+// accumulated into eatom (atomics; one add per CTA that touched the atom), the
+// CTA's partial total goes to part_sums[block], and the last CTA to finish
+// (threadfence + ticket) sums part_sums in block order into *etotal, so the
+// total is deterministic and needs no extra launch.
+// ---------------------------------------------------------------------------
+struct EnergyOut {
+  double* eatom;
+  double* part_sums;   // one per CTA
+  unsigned* ticket;    // zero at launch; reset by the last CTA
+  double* etotal;
 };
 
-template <int T, int J1, int J2, int J>
-__device__ __forceinline__ void y_tuple_rows(const double* __restrict__ sX, int lane, int mb,
-                                             const double* __restrict__ W, double (&accr)[J + 1],
-                                             double (&acci)[J + 1]) {
-  constexpr int NF = c_full_off(T + 1);
-  constexpr int D = (J1 + J2 - J) / 2;
-  constexpr int COFF = c_cg_off(T, J1, J2, J);
-  constexpr int CB = cp_base(T) + COFF;
-  const int lo = max(0, mb + D - J2), hi = min(J1, mb + D);
-  for (int mb1 = lo; mb1 <= hi; ++mb1) {
-    const int mb2 = mb + D - mb1;
-    const double w = __ldg(W + COFF + mb1 * (J2 + 1) + mb2);
-    const double* p1 = sX + (c_full_off(J1) + mb1 * (J1 + 1)) * 32 + lane;
-    const double* p2 = sX + (c_full_off(J2) + mb2 * (J2 + 1)) * 32 + lane;
-    double x1r[J1 + 1], x1i[J1 + 1], x2r[J2 + 1], x2i[J2 + 1];
+__device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_e, bool valid,
+                                                int atom) {
+  // called by one full warp of the CTA
+  const int lane = threadIdx.x & 31;
+  if (valid) atomicAdd(E.eatom + atom, lane_e);
+  double s = valid ? lane_e : 0.0;
 #pragma unroll
-    for (int a = 0; a <= J1; ++a) {
-      x1r[a] = p1[a * 32];
-      x1i[a] = p1[(NF + a) * 32];
-    }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const unsigned nblk = gridDim.x * gridDim.y;
+  const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
+  unsigned t = 0;
+  if (lane == 0) {
+    E.part_sums[bid] = s;
+    __threadfence();
+    t = atomicAdd(E.ticket, 1u);
+  }
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t == nblk - 1) {  // last CTA: deterministic ordered sum
+    __threadfence();
+    double acc = 0.0;
+    for (unsigned b = lane; b < nblk; b += 32) acc += __ldcg(E.part_sums + b);
 #pragma unroll
-    for (int a = 0; a <= J2; ++a) {
-      x2r[a] = p2[a * 32];
-      x2i[a] = p2[(NF + a) * 32];
-    }
-#pragma unroll
-    for (int ma = 0; ma <= J; ++ma) {
-      const int alo = cmax(0, ma + D - J2), ahi = cmin(J1, ma + D);
-      double sr = 0.0, si = 0.0;
-#pragma unroll
-      for (int a1 = alo; a1 <= ahi; ++a1) {
-        const int a2 = ma + D - a1;
-        const double cc = cCP[CB + a1 * (J2 + 1) + a2];
-        const double tr = x1r[a1] * x2r[a2] - x1i[a1] * x2i[a2];
-        const double ti = x1r[a1] * x2i[a2] + x1i[a1] * x2r[a2];
-        sr = fma(cc, tr, sr);
-        si = fma(cc, ti, si);
-      }
-      accr[ma] = fma(w, sr, accr[ma]);
-      acci[ma] = fma(w, si, acci[ma]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      *E.etotal = acc;
+      *E.ticket = 0u;
     }
   }
 }
 
-// Compile-time walk over every coupling tuple (J1 >= J2) that targets J.
-template <int T, int J, int J1, int J2>
-struct YTupleWalk {
-  __device__ __forceinline__ static void run(const double* sX, int lane, int mb, const double* W,
-                                             double (&ar)[J + 1], double (&ai)[J + 1]) {
-    if constexpr (J1 <= T) {
-      if constexpr (J2 <= J1) {
-        constexpr bool ok = (J >= J1 - J2) && (J <= J1 + J2) && (((J1 + J2 - J) & 1) == 0);
-        if constexpr (ok) y_tuple_rows<T, J1, J2, J>(sX, lane, mb, W, ar, ai);
-        YTupleWalk<T, J, J1, J2 + 1>::run(sX, lane, mb, W, ar, ai);
-      } else {
-        YTupleWalk<T, J, J1 + 1, 0>::run(sX, lane, mb, W, ar, ai);
+// ===========================================================================
+// compute_Y  (snap_core.hpp:1085-1200), any twojmax <= 14
+//
+// Lanes = atoms of an AoSoA tile (every lane runs the same loop bounds and
+// reads the same coefficient), TA = 32 atoms per CTA when the half-storage V
+// tile fits in shared memory (2J <= 10), else 16 atoms with the two
+// half-warps splitting the a2 loop.  Each warp owns whole target rows (j, mb)
+// and keeps the row's outputs in registers across every contributing "row
+// pair" item (coupling tuple (j1, j2) -> j, factor rows mb1 of level j1 and
+// mb2 = mb + D - mb1 of level j2, D = (j1+j2-j)/2).  Per item the kernel runs
+// a runtime loop over the elements a2 of the shorter factor row and keeps a
+// sliding register window of the longer row aligned with the outputs:
+//     acc[ma] += C'(a1 = ma + D - a2, a2) * x1[a1] * (w * x2[a2])
+// so each step loads one new x1 element and one x2 element for j+1 complex
+// MACs; the window length j+1 (j/2+1 on the middle row, whose upper half is
+// never read) is a template parameter, so the whole kernel is a handful of
+// small loops (no instruction-cache pressure) while all arithmetic operands
+// stay in registers.  Coefficients C' (v-space CG, zero-padded per a2 row)
+// and the per-item W' factors are host-built (tables.cpp).
+// Output: Y' (v-space, weighted); epilogue E_i = 2/3 sum Re(Y'_s conj V).
+// ===========================================================================
+struct YArgs {
+  const double* V;        // [tile32][2][NH][32]
+  double* Y;              // [tile32][2][NH][32]
+  const int4* items;      // row-pair items: x1 row base, x2 row base, packed dims, coef off
+  const double* itw;      // W' per item
+  const int* row_begin;   // per target row id (j,mb): item range [begin, end)
+  const double* cw;       // windowed C' table
+  const int* tasks;       // [worker][cap] row codes j*64+mb, -1 terminated
+  int task_cap;
+  int nlocal;
+  EnergyOut E;
+};
+
+__device__ __forceinline__ double flip_sign(double x, unsigned mask) {
+  return __hiloint2double(__double2hiint(x) ^ (int)mask, __double2loint(x));
+}
+
+// Element a of factor row X(t, mb, .) from the half-storage tile: stored rows
+// directly, mirrored rows (2 mb > t) through u(t-mb,t-ma) = (-1)^(ma+mb) conj u(mb,ma)
+// (halfint_index.hpp:22-25); the (-1)^mb factor is folded into W'.
+struct RowRef {
+  const double* p;  // re plane element 0 of the row walk (lane offset applied)
+  int step;         // +TA or -TA (doubles)
+  unsigned m;       // 0x80000000 when mirrored
+};
+
+template <int TA, int NH>
+__device__ __forceinline__ void row_load(const RowRef& r, int a, double& re, double& im) {
+  const double* q = r.p + a * r.step;
+  re = q[0];
+  im = q[NH * TA];
+  const unsigned odd = (a & 1) ? 0xffffffffu : 0u;
+  re = flip_sign(re, r.m & odd);
+  im = flip_sign(im, r.m & ~odd);
+}
+
+template <int TA, int NH>
+__device__ __forceinline__ RowRef make_row(const double* sV, int ln, int base, int t, bool mir) {
+  RowRef r;
+  r.p = sV + (size_t)(base + (mir ? t : 0)) * TA + ln;
+  r.step = mir ? -TA : TA;
+  r.m = mir ? 0x80000000u : 0u;
+  return r;
+}
+
+template <int T, int TA, int L>
+__device__ __forceinline__ void y_row_items(const double* __restrict__ sV, int ln, int sub,
+                                            const YArgs& A, int it0, int it1, double (&ar)[L],
+                                            double (&ai)[L]) {
+  constexpr int NH = c_half_off(T + 1);
+  constexpr int SUB = 32 / TA;
+  for (int it = it0; it < it1; ++it) {
+    const int4 m = __ldg(A.items + it);
+    const double w = __ldg(A.itw + it);
+    const int J1 = m.z & 0xff, J2 = (m.z >> 8) & 0xff, D = (m.z >> 16) & 0xff;
+    const bool m1 = (m.z >> 24) & 1, m2 = (m.z >> 25) & 1;
+    const int JW = (m.z >> 26) & 0x1f;  // coefficient row length (j+1)
+    const RowRef r1 = make_row<TA, NH>(sV, ln, m.x, J1, m1);
+    const RowRef r2 = make_row<TA, NH>(sV, ln, m.y, J2, m2);
+    const double* cw = A.cw + m.w;
+    // window: W[ma] = x1[ma + D - a2], a2 starting at `sub`
+    double wr[L], wi[L];
+#pragma unroll
+    for (int ma = 0; ma < L; ++ma) {
+      const int a1 = min(max(ma + D - sub, 0), J1);
+      row_load<TA, NH>(r1, a1, wr[ma], wi[ma]);
+    }
+    for (int a2 = sub; a2 <= J2; a2 += SUB) {
+      double x2r, x2i;
+      row_load<TA, NH>(r2, a2, x2r, x2i);
+      x2r *= w;
+      x2i *= w;
+      const double* c = cw + a2 * JW;
+#pragma unroll
+      for (int ma = 0; ma < L; ++ma) {
+        const double cc = __ldg(c + ma);
+        const double pr = wr[ma] * x2r - wi[ma] * x2i;
+        const double pi = wr[ma] * x2i + wi[ma] * x2r;
+        ar[ma] = fma(cc, pr, ar[ma]);
+        ai[ma] = fma(cc, pi, ai[ma]);
+      }
+      // slide the window by SUB
+#pragma unroll
+      for (int ma = L - 1; ma >= SUB; --ma) {
+        wr[ma] = wr[ma - SUB];
+        wi[ma] = wi[ma - SUB];
+      }
+#pragma unroll
+      for (int ma = 0; ma < SUB && ma < L; ++ma) {
+        const int a1 = min(max(ma + D - a2 - SUB, 0), J1);
+        row_load<TA, NH>(r1, a1, wr[ma], wi[ma]);
       }
     }
   }
+}
+
+// One target row (j, mb), cooperatively: the row's row-pair items are dealt
+// round-robin to the CTA's warps (all warps run the same loop body), partial
+// rows meet in shared memory, and each warp finishes a stripe of the outputs.
+template <int T, int TA, int J, bool MID>
+__device__ __forceinline__ void y_row(const double* __restrict__ sV, double* __restrict__ sred,
+                                      int lane, int w, int nw, int mb, const YArgs& A, int rid,
+                                      double* __restrict__ Yt, double& e_acc) {
+  constexpr int NH = c_half_off(T + 1);
+  constexpr int L = MID ? J / 2 + 1 : J + 1;
+  const int ln = lane % TA, sub = lane / TA;
+  double ar[L], ai[L];
+#pragma unroll
+  for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
+  const int b = __ldg(A.row_begin + rid), e = __ldg(A.row_begin + rid + 1);
+  for (int it = b + w; it < e; it += nw) y_row_items<T, TA, L>(sV, ln, sub, A, it, it + 1, ar, ai);
+#pragma unroll
+  for (int o = TA; o < 32; o <<= 1)
+#pragma unroll
+    for (int m = 0; m < L; ++m) {
+      ar[m] += __shfl_xor_sync(0xffffffffu, ar[m], o);
+      ai[m] += __shfl_xor_sync(0xffffffffu, ai[m], o);
+    }
+  // partial rows -> shared: sred[w][m][re|im][32]
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    sred[((w * L + m) * 2 + 0) * 32 + lane] = ar[m];
+    sred[((w * L + m) * 2 + 1) * 32 + lane] = ai[m];
+  }
+  __syncthreads();
+  const int hb = c_half_off(J) + mb * (J + 1);
+  for (int ma = w; ma <= J; ma += nw) {
+    double yr = 0.0, yi = 0.0;
+    if (ma < L) {
+      for (int q = 0; q < nw; ++q) {
+        yr += sred[((q * L + ma) * 2 + 0) * 32 + lane];
+        yi += sred[((q * L + ma) * 2 + 1) * 32 + lane];
+      }
+      const double wgt = (MID && 2 * ma == J) ? 0.5 : 1.0;
+      yr *= wgt;
+      yi *= wgt;
+      if (sub == 0)
+        e_acc += yr * sV[(hb + ma) * TA + ln] + yi * sV[(NH + hb + ma) * TA + ln];
+    }
+    if (sub == 0) {
+      Yt[(size_t)(hb + ma) * 32] = yr;
+      Yt[(size_t)(NH + hb + ma) * 32] = yi;
+    }
+  }
+  __syncthreads();
+}
+
+template <int T, int TA>
+__global__ void __launch_bounds__(256) k_compute_Y(const YArgs A) {
+  constexpr int NH = c_half_off(T + 1);
+  extern __shared__ double smem[];
+  double* sV = smem;                   // [re|im][half idx][TA atoms]
+  double* sred = smem + 2 * NH * TA;   // [warp][T+1][re|im][32]
+  __shared__ double se[8][32];
+  const int atom0 = blockIdx.x * TA;
+  const double* Vt = A.V + (size_t)(atom0 >> 5) * 2 * NH * 32 + (atom0 & 31);
+  for (int e = threadIdx.x; e < 2 * NH * TA; e += blockDim.x) {
+    const int row = e / TA, ln = e - row * TA;  // row = plane*NH + idx
+    sV[e] = Vt[(size_t)row * 32 + ln];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
+  const int atom = atom0 + (lane % TA);
+  double* Yt = A.Y + (size_t)(atom >> 5) * 2 * NH * 32 + (atom & 31);
+  double e_acc = 0.0;
+  for (int q = 0;; ++q) {
+    const int code = __ldg(tasks + q);
+    if (code < 0) break;
+    const int j = code >> 6, mb = code & 63;
+    const int rid = c_acc_off(j) + mb;  // rows enumerated (j, mb <= j/2)
+    const bool mid = 2 * mb == j;
+#define YROW(JJ)                                                                        \
+  case JJ:                                                                              \
+    if constexpr (JJ <= T) {                                                            \
+      if (mid) y_row<T, TA, JJ, true>(sV, sred, lane, w, nw, mb, A, rid, Yt, e_acc);   \
+      else y_row<T, TA, JJ, false>(sV, sred, lane, w, nw, mb, A, rid, Yt, e_acc);      \
+    }                                                                                   \
+    break;
+    switch (j) {
+      YROW(0) YROW(1) YROW(2) YROW(3) YROW(4) YROW(5) YROW(6) YROW(7)
+      YROW(8) YROW(9) YROW(10) YROW(11) YROW(12) YROW(13) YROW(14)
+      default: break;
+    }
+#undef YROW
+  }
+  // per-atom energy: fixed-order sum over the warps (deterministic)
+  se[w][lane] = e_acc;
+  __syncthreads();
+  if (w == 0) {
+    double s = 0.0;
+    for (int q = 0; q < nw; ++q) s += se[q][lane];
+    energy_epilogue(A.E, (2.0 / 3.0) * s, lane < TA && atom < A.nlocal, atom);
+  }
+}
+
+// ===========================================================================
+// compute_Y, unrolled cooperative variant for 2J <= 8 (snap_core.hpp:1085-1200)
+//
+// The per-tuple (j1, j2) -> j contraction body is fully unrolled (operands in
+// registers, C' coefficients as uniform constant-bank loads: ~85% of the
+// instructions are DFMA/DMUL).  Instruction-cache locality comes from the
+// schedule: all warps of the CTA (one CTA per SM, one 32-atom tile) work on
+// the SAME target row (j, mb) at the same time, each on an LPT-balanced share
+// of the row's row-pair items, so the live code is only the bodies of the
+// tuples targeting j (<= 55 KB at 2J = 8) instead of all 125 (~400 KB).
+// Partial rows meet in shared memory; X is the tile's full mirrored stack.
+// ===========================================================================
+__host__ __device__ constexpr int c_tuple_field(int T, int Q, int f) {
+  int n = 0;
+  for (int j1 = 0; j1 <= T; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) {
+        if (n == Q) return f == 0 ? j1 : (f == 1 ? j2 : j);
+        ++n;
+      }
+  return -1;
+}
+__host__ __device__ constexpr int c_n_tuples(int T) {
+  int n = 0;
+  for (int j1 = 0; j1 <= T; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) ++n;
+  return n;
+}
+// Band limits with an unrolled compute_Y; their C' tables are stacked in
+// constant memory (2J = 7 is left to the windowed kernel to stay < 64 KB).
+__host__ __device__ constexpr bool y_unrolled(int T) { return T <= 8 && T != 7; }
+__host__ __device__ constexpr int cp_base(int T) {
+  int o = 0;
+  for (int s = 0; s < T; ++s)
+    if (y_unrolled(s)) o += c_cg_total(s);
+  return o;
+}
+constexpr int kCpTotal = cp_base(9);
+__constant__ double cCP[kCpTotal];
+
+struct YCArgs {
+  const double* V;      // [tile32][2][NH][32]
+  double* Y;            // [tile32][2][NH][32]
+  const int* expand;    // full idx -> half src code (mirror map)
+  const int4* items;    // {local tuple index within j, mb1, mb2, 0}, per (row, warp)
+  const double* itw;    // W per item
+  const int* rw_begin;  // [row][warp] -> item range start; [row][W] = end
+  int nwarps;           // warps the item split was made for
+  const int* tasks;     // [part][cap] row codes, -1 terminated
+  int task_cap;
+  int nlocal;
+  EnergyOut E;
 };
 
+template <int T, int J1, int J2, int J>
+__device__ __forceinline__ void yc_item(const double* __restrict__ sX, int lane, int mb1,
+                                        int mb2, double w, double (&accr)[J + 1],
+                                        double (&acci)[J + 1]) {
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int D = (J1 + J2 - J) / 2;
+  constexpr int CB = cp_base(T) + c_cg_off(T, J1, J2, J);
+  const double* p1 = sX + (c_full_off(J1) + mb1 * (J1 + 1)) * 32 + lane;
+  const double* p2 = sX + (c_full_off(J2) + mb2 * (J2 + 1)) * 32 + lane;
+  double x1r[J1 + 1], x1i[J1 + 1], x2r[J2 + 1], x2i[J2 + 1];
+#pragma unroll
+  for (int a = 0; a <= J1; ++a) {
+    x1r[a] = p1[a * 32];
+    x1i[a] = p1[(NF + a) * 32];
+  }
+#pragma unroll
+  for (int a = 0; a <= J2; ++a) {
+    x2r[a] = p2[a * 32];
+    x2i[a] = p2[(NF + a) * 32];
+  }
+#pragma unroll
+  for (int ma = 0; ma <= J; ++ma) {
+    const int alo = cmax(0, ma + D - J2), ahi = cmin(J1, ma + D);
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int a1 = alo; a1 <= ahi; ++a1) {
+      const int a2 = ma + D - a1;
+      const double cc = cCP[CB + a1 * (J2 + 1) + a2];
+      const double tr = x1r[a1] * x2r[a2] - x1i[a1] * x2i[a2];
+      const double ti = x1r[a1] * x2i[a2] + x1i[a1] * x2r[a2];
+      sr = fma(cc, tr, sr);
+      si = fma(cc, ti, si);
+    }
+    accr[ma] = fma(w, sr, accr[ma]);
+    acci[ma] = fma(w, si, acci[ma]);
+  }
+}
+
+// L-th coupling tuple (in reference order) whose target is J: field 0/1 = j1/j2.
+__host__ __device__ constexpr int c_tuple_for_j(int T, int J, int L, int f) {
+  int n = 0;
+  for (int j1 = 0; j1 <= T; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2)
+        if (j == J) {
+          if (n == L) return f == 0 ? j1 : j2;
+          ++n;
+        }
+  return -1;
+}
+__host__ __device__ constexpr int c_ntuples_for_j(int T, int J) {
+  int n = 0;
+  for (int j1 = 0; j1 <= T; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) n += (j == J);
+  return n;
+}
+
+// dispatch an item of target row J to its tuple body through one dense
+// switch (a single indirect branch) on the item's local tuple index
 template <int T, int J>
-__device__ __forceinline__ void y_row(const double* sX, int lane, int mb, const YArgs& A,
-                                      double* __restrict__ Yt, double& e_acc) {
+__device__ __forceinline__ void yc_dispatch(int ql, const double* sX, int lane, int mb1, int mb2,
+                                            double w, double (&ar)[J + 1], double (&ai)[J + 1]) {
+#define YCASE(L)                                                                               \
+  case L:                                                                                      \
+    if constexpr (L < c_ntuples_for_j(T, J))                                                   \
+      yc_item<T, c_tuple_for_j(T, J, L, 0), c_tuple_for_j(T, J, L, 1), J>(sX, lane, mb1, mb2, \
+                                                                          w, ar, ai);          \
+    break;
+  switch (ql) {
+    YCASE(0) YCASE(1) YCASE(2) YCASE(3) YCASE(4) YCASE(5) YCASE(6) YCASE(7) YCASE(8) YCASE(9)
+    YCASE(10) YCASE(11) YCASE(12) YCASE(13) YCASE(14) YCASE(15) YCASE(16) YCASE(17) YCASE(18)
+    YCASE(19) YCASE(20) YCASE(21) YCASE(22) YCASE(23) YCASE(24)
+    default: break;
+  }
+#undef YCASE
+}
+
+template <int T, int J>
+__device__ __forceinline__ void yc_row(const double* __restrict__ sX, double* __restrict__ sred,
+                                       int lane, int w, int nw, int mb, int rid, const YCArgs& A,
+                                       double* __restrict__ Yt, double& e_acc) {
   constexpr int NF = c_full_off(T + 1);
   constexpr int NH = c_half_off(T + 1);
   double ar[J + 1], ai[J + 1];
 #pragma unroll
   for (int m = 0; m <= J; ++m) ar[m] = ai[m] = 0.0;
-  YTupleWalk<T, J, 0, 0>::run(sX, lane, mb, A.W, ar, ai);
-  const bool mid = (2 * mb == J);
+  const int* rb = A.rw_begin + rid * (A.nwarps + 1);
+  const int b = __ldg(rb + w), e = __ldg(rb + w + 1);
+  int4 m = make_int4(0, 0, 0, 0);
+  double wt = 0.0;
+  if (b < e) {
+    m = __ldg(A.items + b);
+    wt = __ldg(A.itw + b);
+  }
+  for (int it = b; it < e; ++it) {
+    // prefetch the next item's descriptor while this one computes
+    int4 mn = m;
+    double wn = wt;
+    if (it + 1 < e) {
+      mn = __ldg(A.items + it + 1);
+      wn = __ldg(A.itw + it + 1);
+    }
+    yc_dispatch<T, J>(m.x, sX, lane, m.y, m.z, wt, ar, ai);
+    m = mn;
+    wt = wn;
+  }
+#pragma unroll
+  for (int m = 0; m <= J; ++m) {
+    sred[((w * (J + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
+    sred[((w * (J + 1) + m) * 2 + 1) * 32 + lane] = ai[m];
+  }
+  __syncthreads();
   const int hb = c_half_off(J) + mb * (J + 1);
   const int fb = c_full_off(J) + mb * (J + 1);
-#pragma unroll
-  for (int ma = 0; ma <= J; ++ma) {
-    double wgt = 1.0;
-    if (mid) wgt = (2 * ma < J) ? 1.0 : ((2 * ma == J) ? 0.5 : 0.0);
-    const double yr = ar[ma] * wgt, yi = ai[ma] * wgt;
+  const bool mid = 2 * mb == J;
+  for (int ma = w; ma <= J; ma += nw) {
+    double yr = 0.0, yi = 0.0;
+    for (int q = 0; q < nw; ++q) {
+      yr += sred[((q * (J + 1) + ma) * 2 + 0) * 32 + lane];
+      yi += sred[((q * (J + 1) + ma) * 2 + 1) * 32 + lane];
+    }
+    const double wgt = mid ? ((2 * ma < J) ? 1.0 : ((2 * ma == J) ? 0.5 : 0.0)) : 1.0;
+    yr *= wgt;
+    yi *= wgt;
+    e_acc += yr * sX[(fb + ma) * 32 + lane] + yi * sX[(NF + fb + ma) * 32 + lane];
     Yt[(size_t)(hb + ma) * 32] = yr;
     Yt[(size_t)(NH + hb + ma) * 32] = yi;
-    e_acc += yr * sX[(fb + ma) * 32 + lane] + yi * sX[(NF + fb + ma) * 32 + lane];
   }
+  __syncthreads();
 }
 
 template <int T>
-__global__ void __launch_bounds__(512, 1) k_compute_Y_spec(const YArgs A) {
+__global__ void __launch_bounds__(384, 1) k_compute_Y_unrolled(const YCArgs A) {
   constexpr int NF = c_full_off(T + 1);
   constexpr int NH = c_half_off(T + 1);
-  extern __shared__ double sX[];  // [2][NF][32]
+  extern __shared__ double smem[];
+  double* sX = smem;                  // [re|im][full idx][32]
+  double* sred = smem + 2 * NF * 32;  // [warp][T+1][re|im][32]
+  __shared__ double se[12][32];
   const int tile = blockIdx.x;
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
   for (int e = threadIdx.x; e < NF * 32; e += blockDim.x) {
@@ -503,139 +832,33 @@ __global__ void __launch_bounds__(512, 1) k_compute_Y_spec(const YArgs A) {
     sX[(NF + f) * 32 + ln] = im;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int worker = blockIdx.y * (blockDim.x >> 5) + w;
-  const int* tasks = A.tasks + (size_t)worker * A.task_cap;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
   double* Yt = A.Y + (size_t)tile * 2 * NH * 32 + lane;
   double e_acc = 0.0;
   for (int q = 0;; ++q) {
     const int code = __ldg(tasks + q);
     if (code < 0) break;
     const int j = code >> 6, mb = code & 63;
+    const int rid = c_acc_off(j) + mb;
+#define YCROW(JJ)                                                                 \
+  case JJ:                                                                        \
+    if constexpr (JJ <= T) yc_row<T, JJ>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc); \
+    break;
     switch (j) {
-      case 0: y_row<T, 0>(sX, lane, mb, A, Yt, e_acc); break;
-      case 1: if constexpr (T >= 1) y_row<T, 1>(sX, lane, mb, A, Yt, e_acc); break;
-      case 2: if constexpr (T >= 2) y_row<T, 2>(sX, lane, mb, A, Yt, e_acc); break;
-      case 3: if constexpr (T >= 3) y_row<T, 3>(sX, lane, mb, A, Yt, e_acc); break;
-      case 4: if constexpr (T >= 4) y_row<T, 4>(sX, lane, mb, A, Yt, e_acc); break;
-      case 5: if constexpr (T >= 5) y_row<T, 5>(sX, lane, mb, A, Yt, e_acc); break;
-      case 6: if constexpr (T >= 6) y_row<T, 6>(sX, lane, mb, A, Yt, e_acc); break;
-      case 7: if constexpr (T >= 7) y_row<T, 7>(sX, lane, mb, A, Yt, e_acc); break;
-      case 8: if constexpr (T >= 8) y_row<T, 8>(sX, lane, mb, A, Yt, e_acc); break;
+      YCROW(0) YCROW(1) YCROW(2) YCROW(3) YCROW(4) YCROW(5) YCROW(6) YCROW(7) YCROW(8)
       default: break;
     }
+#undef YCROW
   }
-  const int atom = tile * 32 + lane;
-  if (atom < A.nlocal) atomicAdd(A.eatom + atom, (2.0 / 3.0) * e_acc);
-}
-
-// ===========================================================================
-// compute_Y, generic (any twojmax <= 14): per target element, runtime loops,
-// u-space tile in shared memory with on-the-fly mirror (UtotView::get,
-// snap_core.hpp:190-199).  TA atoms per CTA tile, 32/TA sublanes split the
-// mb1 loop.  Used for twojmax outside the specialized set.
-// ===========================================================================
-struct YGArgs {
-  const double* V;
-  double* Y;
-  const double* cg;        // CG table (reference layout)
-  const double* bfold;     // fold_beta per tuple
-  const int* tuples;       // [ntup][5] j1 j2 j elem cg_off
-  const int* elem_info;    // [nelem][6]
-  const int* elem_tups;
-  const int* tasks;        // [worker][cap]
-  int task_cap;
-  const double* hf;        // f per half idx
-  const double* ywgt;      // stored-Y weight per half idx
-  const int* half_off;     // T+2
-  int T, NH, nlocal;
-  double* eatom;
-};
-
-template <int TA>
-__global__ void __launch_bounds__(256) k_compute_Y_gen(const YGArgs A) {
-  constexpr int SUB = 32 / TA;
-  extern __shared__ double sU[];  // [2][NH][TA] u-space
-  const int NH = A.NH;
-  const int a0 = blockIdx.x * TA;  // first atom of the CTA tile
-  for (int e = threadIdx.x; e < NH * TA; e += blockDim.x) {
-    const int h = e / TA, ln = e - h * TA;
-    const int atom = a0 + ln;
-    const double* Vt = A.V + (size_t)(atom >> 5) * 2 * NH * 32 + (atom & 31);
-    const double inv = 1.0 / A.hf[h];
-    sU[h * TA + ln] = Vt[(size_t)h * 32] * inv;
-    sU[(NH + h) * TA + ln] = Vt[(size_t)(NH + h) * 32] * inv;
-  }
+  se[w][lane] = e_acc;
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int ln = lane % TA, sub = lane / TA;
-  const int worker = blockIdx.y * (blockDim.x >> 5) + w;
-  const int* tasks = A.tasks + (size_t)worker * A.task_cap;
-  const int atom = a0 + ln;
-  double* Yt = A.Y + (size_t)(atom >> 5) * 2 * NH * 32 + (atom & 31);
-  double e_acc = 0.0;
-  auto getU = [&](int t, int mb, int ma, double& re, double& im) {
-    const bool mir = 2 * mb > t;
-    const int mbs = mir ? t - mb : mb, mas = mir ? t - ma : ma;
-    const int h = A.half_off[t] + mbs * (t + 1) + mas;
-    re = sU[h * TA + ln];
-    im = sU[(NH + h) * TA + ln];
-    if (mir) {
-      const double sg = ((ma + mb) & 1) ? -1.0 : 1.0;
-      re *= sg;
-      im *= -sg;
-    }
-  };
-  for (int q = 0;; ++q) {
-    const int eid = __ldg(A.tasks + (size_t)worker * A.task_cap + q);
-    if (eid < 0) break;
-    const int* ei = A.elem_info + eid * 6;
-    const int j = ei[0], mb = ei[1], ma = ei[2], h = ei[3];
-    double yr = 0.0, yi = 0.0;
-    for (int tq = ei[4]; tq < ei[5]; ++tq) {
-      const int tid = A.elem_tups[tq];
-      const int* tp = A.tuples + tid * 5;
-      const int j1 = tp[0], j2 = tp[1], cgo = tp[4];
-      const int D = (j1 + j2 - j) / 2;
-      const int mblo = max(0, mb + D - j2), mbhi = min(j1, mb + D);
-      const int malo = max(0, ma + D - j2), mahi = min(j1, ma + D);
-      double zr = 0.0, zi = 0.0;
-      for (int mb1 = mblo + sub; mb1 <= mbhi; mb1 += SUB) {
-        const int mb2 = mb + D - mb1;
-        double sr = 0.0, si = 0.0;
-        for (int ma1 = malo; ma1 <= mahi; ++ma1) {
-          const int ma2 = ma + D - ma1;
-          double u1r, u1i, u2r, u2i;
-          getU(j1, mb1, ma1, u1r, u1i);
-          getU(j2, mb2, ma2, u2r, u2i);
-          const double cc = __ldg(A.cg + cgo + ma1 * (j2 + 1) + ma2);
-          sr += cc * (u1r * u2r - u1i * u2i);
-          si += cc * (u1r * u2i + u1i * u2r);
-        }
-        const double cb = __ldg(A.cg + cgo + mb1 * (j2 + 1) + mb2);
-        zr += cb * sr;
-        zi += cb * si;
-      }
-      const double bf = __ldg(A.bfold + tid);
-      yr += bf * zr;
-      yi += bf * zi;
-    }
-#pragma unroll
-    for (int o = TA; o < 32; o <<= 1) {
-      yr += __shfl_xor_sync(0xffffffffu, yr, o);
-      yi += __shfl_xor_sync(0xffffffffu, yi, o);
-    }
-    const double sc = A.ywgt[h] / A.hf[h];
-    const double ysr = yr * sc, ysi = yi * sc;
-    if (sub == 0) {
-      Yt[(size_t)h * 32] = ysr;
-      Yt[(size_t)(NH + h) * 32] = ysi;
-      double ur, ui;
-      getU(j, mb, ma, ur, ui);
-      e_acc += A.hf[h] * (ysr * ur + ysi * ui);  // Re(Y'_s conj V), V = f u
-    }
+  if (w == 0) {
+    double s = 0.0;
+    for (int q = 0; q < nw; ++q) s += se[q][lane];
+    const int atom = tile * 32 + lane;
+    energy_epilogue(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
   }
-  if (sub == 0 && atom < A.nlocal) atomicAdd(A.eatom + atom, (2.0 / 3.0) * e_acc);
 }
 
 // ===========================================================================
@@ -654,6 +877,7 @@ struct DEArgs {
   GeoParams gp;
   const double* Y;  // Y' stored
   double* dedr;     // [nlocal*stride][3]
+  double* forces;   // natoms_total x 3, or null: fused scatter (snap_core.hpp:1380-1388)
   int nslots;       // nlocal*stride
 };
 
@@ -829,8 +1053,21 @@ __global__ void __launch_bounds__(DECfg<T>::WARPS * 32, (T <= 8 ? 2 : 3))
   }
   if (valid && r == 0) {
     double* o = A.dedr + (size_t)p * 3;
+    double de[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) o[d] = 2.0 * (g.dsf[d] * Au + g.sfac * Ad[d]);
+    for (int d = 0; d < 3; ++d) {
+      de[d] = 2.0 * (g.dsf[d] * Au + g.sfac * Ad[d]);
+      o[d] = de[d];
+    }
+    if (A.forces) {  // F_i += dE, F_nbr -= dE
+      double* fi = A.forces + (size_t)(A.pr.atom_lo + i) * 3;
+      double* fj = A.forces + (size_t)A.pr.nbr[p] * 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        atomicAdd(fi + d, de[d]);
+        atomicAdd(fj + d, -de[d]);
+      }
+    }
   }
 }
 
@@ -876,6 +1113,22 @@ __global__ void __launch_bounds__(1024) k_energy_total(const double* eatom, int 
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = red[0];
+}
+
+// FP64 issue-rate probe: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters, double s) {
+  double a[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = threadIdx.x * 1e-3 + q;
+  const double b = 1.0 - 1e-9 * s, c = 1e-7 * s;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = fma(a[q], b, c);
+  }
+  double r = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) r += a[q];
+  if (r == 1234.5678) out[0] = r;  // keep the chains alive
 }
 
 }  // namespace snapgpu

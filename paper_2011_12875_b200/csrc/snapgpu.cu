@@ -43,7 +43,7 @@ struct StateErr {
   std::string msg;
 };
 
-void require(bool ok, const std::string& m) {
+inline void require(bool ok, const char* m) {
   if (!ok) throw InvalidArg{m};
 }
 
@@ -81,11 +81,14 @@ struct snapgpu_ctx {
   std::vector<double> cg, hf, ywgt;
 
   // device tables
-  DevBuf<double> d_weights, d_W, d_cg, d_bfold, d_hf, d_ywgt;
-  DevBuf<int> d_expand, d_tasks, d_tuples, d_einfo, d_etups, d_halfoff;
+  DevBuf<double> d_weights, d_itw, d_cw, d_citw;
+  DevBuf<int4> d_items, d_citems;
+  DevBuf<int> d_rowbeg, d_tasks, d_expand, d_rwbeg;
+  YPlan yplan;
+  YCoopPlan ycplan;
   int task_cap = 0;
-  int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;
-  int y_gen_ta = 32;
+  int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
+  int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
 
   // problem shape
   std::vector<int> h_numneigh;
@@ -94,12 +97,15 @@ struct snapgpu_ctx {
 
   // device arrays
   DevBuf<int> d_numneigh, d_nbr, d_types;
-  DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal;
+  DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal, d_part;
+  DevBuf<unsigned> d_ticket;
 
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   bool graph_valid = false;
+
+  bool fuse_scatter = true;  // dE kernel scatters forces (reference `fused` variant)
 
   // timing
   bool timing = false;
@@ -136,21 +142,6 @@ int guarded(snapgpu_ctx* c, F&& f) {
     (c ? c->err : g_err) = e.what();
     return SNAPGPU_EPIPELINE;
   }
-}
-
-// ---------------------------------------------------------------------------
-// constant-memory upload of the specialized C' tables (once per device, T)
-// ---------------------------------------------------------------------------
-void upload_cprime(int device, int T, const IndexMaps& m, const std::vector<double>& cg) {
-  static std::mutex mu;
-  static std::vector<std::pair<int, int>> done;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& d : done)
-    if (d.first == device && d.second == T) return;
-  const std::vector<double> cp = cprime_table(m, cg);
-  CK(cudaMemcpyToSymbol(cCP, cp.data(), cp.size() * sizeof(double),
-                        static_cast<size_t>(cp_base(T)) * sizeof(double)));
-  done.push_back({device, T});
 }
 
 // ---------------------------------------------------------------------------
@@ -213,59 +204,70 @@ struct LaunchU {
   }
 };
 
+EnergyOut energy_out(snapgpu_ctx* c) {
+  EnergyOut E;
+  E.eatom = c->d_eatom.p;
+  E.part_sums = c->d_part.p;
+  E.ticket = c->d_ticket.p;
+  E.etotal = c->d_etotal.p;
+  return E;
+}
+
 template <int T>
 struct LaunchY {
+  template <int TA>
+  static void launch(snapgpu_ctx* c) {
+    constexpr int NH = c_half_off(T + 1);
+    YArgs a;
+    a.V = c->d_V.p;
+    a.Y = c->d_Y.p;
+    a.items = c->d_items.p;
+    a.itw = c->d_itw.p;
+    a.row_begin = c->d_rowbeg.p;
+    a.cw = c->d_cw.p;
+    a.tasks = c->d_tasks.p;
+    a.task_cap = c->task_cap;
+    a.nlocal = c->nlocal;
+    a.E = energy_out(c);
+    const size_t smem = sizeof(double) * (2 * NH * TA + (size_t)c->y_warps * (T + 1) * 2 * 32);
+    CK(cudaFuncSetAttribute(k_compute_Y<T, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    dim3 grid((c->ntiles * 32) / TA, c->y_parts_used);
+    k_compute_Y<T, TA><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+    CK(cudaGetLastError());
+  }
   static void go(snapgpu_ctx* c) {
-    if constexpr (y_specialized(T)) {
+    constexpr int NH = c_half_off(T + 1);
+    if constexpr (y_unrolled(T)) {
       constexpr int NF = c_full_off(T + 1);
-      YArgs a;
+      YCArgs a;
       a.V = c->d_V.p;
       a.Y = c->d_Y.p;
-      a.W = c->d_W.p;
       a.expand = c->d_expand.p;
+      a.items = c->d_citems.p;
+      a.itw = c->d_citw.p;
+      a.rw_begin = c->d_rwbeg.p;
+      a.nwarps = c->ycplan.warps;
       a.tasks = c->d_tasks.p;
       a.task_cap = c->task_cap;
       a.nlocal = c->nlocal;
-      a.eatom = c->d_eatom.p;
-      const size_t smem = sizeof(double) * 2 * NF * 32;
-      CK(cudaFuncSetAttribute(k_compute_Y_spec<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
+      a.E = energy_out(c);
+      const size_t smem = sizeof(double) * (2 * NF * 32 + (size_t)c->y_warps * (T + 1) * 2 * 32);
+      CK(cudaFuncSetAttribute(k_compute_Y_unrolled<T>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       dim3 grid(c->ntiles, c->y_parts_used);
-      k_compute_Y_spec<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+      k_compute_Y_unrolled<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
       CK(cudaGetLastError());
-    } else {
-      YGArgs a;
-      a.V = c->d_V.p;
-      a.Y = c->d_Y.p;
-      a.cg = c->d_cg.p;
-      a.bfold = c->d_bfold.p;
-      a.tuples = c->d_tuples.p;
-      a.elem_info = c->d_einfo.p;
-      a.elem_tups = c->d_etups.p;
-      a.tasks = c->d_tasks.p;
-      a.task_cap = c->task_cap;
-      a.hf = c->d_hf.p;
-      a.ywgt = c->d_ywgt.p;
-      a.half_off = c->d_halfoff.p;
-      a.T = T;
-      a.NH = c->maps.nhalf;
-      a.nlocal = c->nlocal;
-      a.eatom = c->d_eatom.p;
-      const int TA = c->y_gen_ta;
-      const size_t smem = sizeof(double) * 2 * (size_t)a.NH * TA;
-      const int ncta = (c->ntiles * 32) / TA;
-      dim3 grid(ncta, c->y_parts_used);
-      if (TA == 32) {
-        CK(cudaFuncSetAttribute(k_compute_Y_gen<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-        k_compute_Y_gen<32><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
-      } else {
-        CK(cudaFuncSetAttribute(k_compute_Y_gen<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-        k_compute_Y_gen<16><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
-      }
-      CK(cudaGetLastError());
+      return;
     }
+    constexpr int RED = 8 * (T + 1) * 2 * 32 * 8;
+    if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
+      if (c->y_ta == 32) return launch<32>(c);
+    }
+    if constexpr (2 * NH * 16 * 8 + RED <= 200 * 1024) {
+      if (c->y_ta >= 16) return launch<16>(c);
+    }
+    return launch<8>(c);
   }
 };
 
@@ -278,6 +280,7 @@ struct LaunchDE {
     a.gp = c->gp;
     a.Y = c->d_Y.p;
     a.dedr = c->d_dedr.p;
+    a.forces = c->fuse_scatter ? c->d_forces.p : nullptr;
     a.nslots = c->nlocal * c->stride;
     const int per_block = C::WARPS * C::PPW;
     const int blocks = (a.nslots + per_block - 1) / per_block;
@@ -288,46 +291,77 @@ struct LaunchDE {
   }
 };
 
-// Y work split: parts per tile so that small problems still fill the SMs.
+// compute_Y work split: TA atoms per CTA (32 when the V tile fits, smaller
+// tiles for small problems so the SMs fill), W warps per CTA owning target
+// rows, and P "parts" of the row list per tile when tiles are still scarce.
+void build_ycoop(snapgpu_ctx* c);
+
 void plan_y(snapgpu_ctx* c) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  const bool spec = y_specialized(c->T);
-  int units = spec ? c->ntiles : (c->ntiles * 32) / c->y_gen_ta;
-  int parts = c->y_parts;
-  if (parts <= 0) parts = std::max(1, std::min(8, nsm / std::max(1, units)));
-  c->y_parts_used = parts;
-  const int workers = parts * c->y_warps;
-  if (spec) {
-    std::vector<int> tasks = y_row_tasks(c->maps, workers, &c->task_cap);
+  if (y_unrolled(c->T)) {  // one 32-atom tile per CTA, all warps per row
+    if (c->ycplan.warps != c->y_warps) build_ycoop(c);
+    int parts = c->y_parts;
+    // one CTA per SM: never exceed a single wave
+    if (parts <= 0) parts = std::max(1, std::min(8, nsm / std::max(1, c->ntiles)));
+    c->y_parts_used = parts;
+    std::vector<int> tasks = y_row_schedule(c->maps, c->ycplan.row_cost, parts, &c->task_cap);
     c->d_tasks.alloc(tasks.size());
     CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
-  } else {
-    GenericYPlan gpn = generic_y_plan(c->maps, workers);
-    c->task_cap = gpn.cap;
-    c->d_tasks.alloc(gpn.elem_tasks.size());
-    CK(cudaMemcpy(c->d_tasks.p, gpn.elem_tasks.data(), gpn.elem_tasks.size() * sizeof(int),
-                  cudaMemcpyHostToDevice));
-    c->d_einfo.alloc(gpn.elem_info.size());
-    CK(cudaMemcpy(c->d_einfo.p, gpn.elem_info.data(), gpn.elem_info.size() * sizeof(int),
-                  cudaMemcpyHostToDevice));
-    c->d_etups.alloc(std::max<size_t>(1, gpn.elem_tups.size()));
-    CK(cudaMemcpy(c->d_etups.p, gpn.elem_tups.data(), gpn.elem_tups.size() * sizeof(int),
-                  cudaMemcpyHostToDevice));
+    return;
   }
+  int ta = c->y_ta_req > 0 ? std::min(c->y_ta_req, c->y_ta_max) : c->y_ta_max;
+  if (c->y_ta_req <= 0)
+    while (ta > 16 && (c->ntiles * 32) / ta < nsm) ta /= 2;  // small N: more, thinner CTAs
+  c->y_ta = ta;
+  const int units = (c->ntiles * 32) / ta;
+  int parts = c->y_parts;
+  if (parts <= 0) parts = std::max(1, std::min(8, (2 * nsm + units - 1) / std::max(1, units)));
+  c->y_parts_used = parts;
+  const int workers = parts;  // all warps of a CTA cooperate on each row
+  std::vector<int> tasks = y_row_schedule(c->maps, c->yplan.row_cost, workers, &c->task_cap);
+  c->d_tasks.alloc(tasks.size());
+  CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
 }
 
 void upload_beta(snapgpu_ctx* c) {
-  const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data());
-  c->d_W.alloc(std::max<size_t>(1, W.size()));
-  CK(cudaMemcpy(c->d_W.p, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice));
-  std::vector<double> bf(c->maps.tuples.size());
-  for (size_t q = 0; q < bf.size(); ++q) {
-    const Tuple& tp = c->maps.tuples[q];
-    bf[q] = fold_beta(c->maps, c->beta.data(), tp.j1, tp.j2, tp.j);
+  if (y_unrolled(c->T)) {
+    const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
+    const std::vector<double> itw = ycoop_weights(c->ycplan, c->maps, W);
+    c->d_citw.alloc(std::max<size_t>(1, itw.size()));
+    CK(cudaMemcpy(c->d_citw.p, itw.data(), itw.size() * sizeof(double),
+                  cudaMemcpyHostToDevice));
+    return;
   }
-  c->d_bfold.alloc(std::max<size_t>(1, bf.size()));
-  CK(cudaMemcpy(c->d_bfold.p, bf.data(), bf.size() * sizeof(double), cudaMemcpyHostToDevice));
+  const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), true);
+  const std::vector<double> itw = y_item_weights(c->maps, W);
+  c->d_itw.alloc(std::max<size_t>(1, itw.size()));
+  CK(cudaMemcpy(c->d_itw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+void build_ycoop(snapgpu_ctx* c) {
+  c->ycplan = ycoop_plan(c->maps, c->y_warps);
+  std::vector<int4> it(c->ycplan.items.size());
+  for (size_t q = 0; q < it.size(); ++q)
+    it[q] = make_int4(c->ycplan.items[q][3], c->ycplan.items[q][1], c->ycplan.items[q][2], 0);
+  c->d_citems.alloc(std::max<size_t>(1, it.size()));
+  CK(cudaMemcpy(c->d_citems.p, it.data(), it.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  c->d_rwbeg.alloc(c->ycplan.rw_begin.size());
+  CK(cudaMemcpy(c->d_rwbeg.p, c->ycplan.rw_begin.data(), c->ycplan.rw_begin.size() * sizeof(int),
+                cudaMemcpyHostToDevice));
+  upload_beta(c);
+}
+
+void upload_cprime(int device, int T, const IndexMaps& m, const std::vector<double>& cg) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == device && d.second == T) return;
+  const std::vector<double> cp = cprime_table(m, cg);
+  CK(cudaMemcpyToSymbol(cCP, cp.data(), cp.size() * sizeof(double),
+                        static_cast<size_t>(cp_base(T)) * sizeof(double)));
+  done.push_back({device, T});
 }
 
 void launch_U(snapgpu_ctx* c) {
@@ -335,11 +369,20 @@ void launch_U(snapgpu_ctx* c) {
 }
 void launch_Y(snapgpu_ctx* c) {
   CK(cudaMemsetAsync(c->d_eatom.p, 0, sizeof(double) * std::max(1, c->nlocal), c->stream));
-  if (c->nlocal > 0) dispatch_T<LaunchY>(c->T, c);
-  k_energy_total<<<1, 1024, 0, c->stream>>>(c->d_eatom.p, c->nlocal, c->d_etotal.p);
-  CK(cudaGetLastError());
+  if (c->nlocal > 0) {
+    dispatch_T<LaunchY>(c->T, c);  // energy total in the kernel's last CTA
+  } else {
+    CK(cudaMemsetAsync(c->d_etotal.p, 0, sizeof(double), c->stream));
+  }
 }
 void launch_dE(snapgpu_ctx* c) {
+  // Fusing the scatter into the dE kernel saves a launch for small problems;
+  // for large ones the separate RED kernel is cheaper than atomics issued
+  // from the latency-bound dE kernel.
+  c->fuse_scatter = (size_t)c->nlocal * c->stride <= (1u << 18);
+  if (c->fuse_scatter)
+    CK(cudaMemsetAsync(c->d_forces.p, 0, sizeof(double) * 3 * std::max(1, c->natoms_total),
+                       c->stream));
   if (c->nlocal > 0) dispatch_T<LaunchDE>(c->T, c);
 }
 void launch_scatter(snapgpu_ctx* c) {
@@ -406,6 +449,9 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
     c->d_forces.alloc((size_t)std::max(1, natoms_total) * 3);
     c->d_eatom.alloc(std::max(1, nlocal));
     c->d_etotal.alloc(1);
+    c->d_part.alloc((size_t)std::max(1, ntiles) * 4 * 8 + 64);  // >= Y grid size
+    c->d_ticket.alloc(1);
+    CK(cudaMemsetAsync(c->d_ticket.p, 0, sizeof(unsigned), c->stream));
     const bool grow = vsz > c->d_V.n;
     c->d_V.alloc(vsz);
     c->d_Y.alloc(vsz);
@@ -451,7 +497,7 @@ void run_direct(snapgpu_ctx* c) {
   record(c, 2);
   launch_dE(c);
   record(c, 3);
-  launch_scatter(c);
+  if (!c->fuse_scatter) launch_scatter(c);
   record(c, 4);
 }
 
@@ -521,17 +567,27 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
       CK(cudaMemcpy(buf.p, v.data(), v.size() * sizeof(E), cudaMemcpyHostToDevice));
     };
     up(c->d_weights, c->weights);
-    up(c->d_cg, c->cg);
-    up(c->d_hf, c->hf);
-    up(c->d_ywgt, c->ywgt);
-    up(c->d_expand, full_expand_map(c->maps));
-    up(c->d_halfoff, c->maps.half_off);
-    std::vector<int> tup;
-    for (const Tuple& tp : c->maps.tuples) tup.insert(tup.end(), {tp.j1, tp.j2, tp.j, tp.elem_off, tp.cg_off});
-    up(c->d_tuples, tup);
-    upload_beta(c);
-    if (y_specialized(twojmax)) upload_cprime(device, twojmax, c->maps, c->cg);
-    c->y_gen_ta = (2.0 * c->maps.nhalf * 32 * 8 <= 200.0 * 1024) ? 32 : 16;
+    c->yplan = y_plan(c->maps, cprime_table(c->maps, c->cg));
+    std::vector<int4> it(c->yplan.items.size());
+    for (size_t q = 0; q < it.size(); ++q)
+      it[q] = make_int4(c->yplan.items[q][0], c->yplan.items[q][1], c->yplan.items[q][2],
+                        c->yplan.items[q][3]);
+    up(c->d_items, it);
+    up(c->d_rowbeg, c->yplan.row_begin);
+    up(c->d_cw, c->yplan.cw);
+    if (y_unrolled(twojmax)) {
+      c->y_warps = 12;
+      up(c->d_expand, full_expand_map(c->maps));
+      upload_cprime(device, twojmax, c->maps, c->cg);
+      build_ycoop(c);  // uploads the beta-dependent item weights
+    } else {
+      upload_beta(c);
+    }
+    const int nh = c->maps.nhalf;
+    // V tile + the cross-warp row buffer (8 warps) must fit in shared memory
+    const double red = 8.0 * (twojmax + 1) * 2 * 32 * 8;
+    c->y_ta_max = (2.0 * nh * 32 * 8 + red <= 200.0 * 1024) ? 32
+                  : ((2.0 * nh * 16 * 8 + red <= 200.0 * 1024) ? 16 : 8);
     *out = c;
   });
   if (rc != SNAPGPU_OK && c) {
@@ -548,17 +604,15 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   c->d_weights.release();
-  c->d_W.release();
-  c->d_cg.release();
-  c->d_bfold.release();
-  c->d_hf.release();
-  c->d_ywgt.release();
+  c->d_itw.release();
+  c->d_cw.release();
+  c->d_items.release();
+  c->d_rowbeg.release();
+  c->d_citems.release();
+  c->d_citw.release();
   c->d_expand.release();
+  c->d_rwbeg.release();
   c->d_tasks.release();
-  c->d_tuples.release();
-  c->d_einfo.release();
-  c->d_etups.release();
-  c->d_halfoff.release();
   c->d_numneigh.release();
   c->d_nbr.release();
   c->d_types.release();
@@ -569,6 +623,8 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_forces.release();
   c->d_eatom.release();
   c->d_etotal.release();
+  c->d_part.release();
+  c->d_ticket.release();
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return SNAPGPU_OK;
@@ -797,6 +853,56 @@ int snapgpu_get_dedr(snapgpu_ctx* c, double* out) {
   });
 }
 
+int snapgpu_get_forces_device(snapgpu_ctx* c, double* dst) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_dE, "get_forces_device before the force pass");
+    require(dst != nullptr, "null output");
+    CK(cudaMemcpyAsync(dst, c->d_forces.p, sizeof(double) * 3 * c->natoms_total,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+int snapgpu_get_energy_device(snapgpu_ctx* c, double* eatom, double* etotal) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_Y, "get_energy_device before compute_Y");
+    if (eatom && c->nlocal > 0)
+      CK(cudaMemcpyAsync(eatom, c->d_eatom.p, sizeof(double) * c->nlocal,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    if (etotal)
+      CK(cudaMemcpyAsync(etotal, c->d_etotal.p, sizeof(double), cudaMemcpyDeviceToDevice,
+                         c->stream));
+  });
+}
+
+int snapgpu_fp64_peak(int device, int iters, double* tflops, double* ms) {
+  return guarded(nullptr, [&] {
+    CK(cudaSetDevice(device));
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    double* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(double)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = nsm * 8, threads = 256;
+    k_fp64_peak<<<blocks, threads>>>(d, 1000, 1.0);  // warm-up
+    CK(cudaEventRecord(e0));
+    k_fp64_peak<<<blocks, threads>>>(d, iters, 1.0);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    const double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+    if (tflops) *tflops = flops / (t * 1e-3) / 1e12;
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+  });
+}
+
 int snapgpu_device_outputs(snapgpu_ctx* c, double** forces, double** eatom, double** etotal) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
@@ -818,13 +924,16 @@ int snapgpu_stage_times(snapgpu_ctx* c, float* out4) {
   return SNAPGPU_OK;
 }
 
-int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int de_warps) {
+int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int y_tile_atoms) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    require(y_warps >= 0 && y_warps <= 16, "tune: y_warps in [0,16]");
+    require(y_warps >= 0 && y_warps <= (y_unrolled(c->T) ? 12 : 8),
+            "tune: y_warps in [0,12] (2J <= 8) or [0,8]");
+    require(y_tile_atoms == 0 || y_tile_atoms == 8 || y_tile_atoms == 16 || y_tile_atoms == 32,
+            "tune: y_tile_atoms in {0, 8, 16, 32}");
     if (y_warps > 0) c->y_warps = y_warps;
     c->y_parts = y_parts;
-    c->de_warps = de_warps;
+    c->y_ta_req = y_tile_atoms;
     invalidate_graph(c);
     if (c->have_lists) plan_y(c);
   });

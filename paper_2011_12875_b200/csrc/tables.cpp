@@ -140,7 +140,7 @@ std::vector<double> cprime_table(const IndexMaps& m, const std::vector<double>& 
 }
 
 std::vector<double> w_table(const IndexMaps& m, const std::vector<double>& cg,
-                            const double* beta) {
+                            const double* beta, bool mirror_signs) {
   std::vector<double> out(m.cgtot, 0.0);
   auto G = [](int t, int mm) { return g_scale(t, std::min(mm, t - mm)); };
   for (const Tuple& tp : m.tuples) {
@@ -151,7 +151,12 @@ std::vector<double> w_table(const IndexMaps& m, const std::vector<double>& cg,
         const int mb = mb1 + mb2 - D;
         const int idx = tp.cg_off + mb1 * (tp.j2 + 1) + mb2;
         if (mb < 0 || 2 * mb > tp.j) continue;
-        out[idx] = bf * cg[idx] / (G(tp.j1, mb1) * G(tp.j2, mb2) * g_scale(tp.j, mb));
+        double s = 1.0;
+        if (mirror_signs) {  // (-1)^mb of mirrored rows (halfint_index.hpp:22-25)
+          if (2 * mb1 > tp.j1 && (mb1 & 1)) s = -s;
+          if (2 * mb2 > tp.j2 && (mb2 & 1)) s = -s;
+        }
+        out[idx] = s * bf * cg[idx] / (G(tp.j1, mb1) * G(tp.j2, mb2) * g_scale(tp.j, mb));
       }
   }
   return out;
@@ -196,26 +201,6 @@ std::vector<int> full_expand_map(const IndexMaps& m) {
   return out;
 }
 
-// Cost of one target row (j, mb) of compute_Y in FP64 instructions per atom:
-// per contributing (tuple, mb1): 6 per complex MAC of the row body, 2 per
-// output of the row update, plus the row loads.
-static double y_row_cost(const IndexMaps& m, int j, int mb) {
-  double c = 0.0;
-  for (const Tuple& tp : m.tuples) {
-    if (tp.j != j) continue;
-    const int D = (tp.j1 + tp.j2 - tp.j) / 2;
-    const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
-    if (hi < lo) continue;
-    int macs = 0;
-    for (int ma = 0; ma <= j; ++ma) {
-      const int alo = std::max(0, ma + D - tp.j2), ahi = std::min(tp.j1, ma + D);
-      macs += std::max(0, ahi - alo + 1);
-    }
-    c += (hi - lo + 1) * (6.0 * macs + 2.0 * (j + 1) + 2.0 * (tp.j1 + tp.j2 + 2));
-  }
-  return c;
-}
-
 static std::vector<std::vector<int>> lpt(const std::vector<std::pair<double, int>>& items,
                                          int workers) {
   std::vector<std::pair<double, int>> sorted = items;
@@ -234,10 +219,122 @@ static std::vector<std::vector<int>> lpt(const std::vector<std::pair<double, int
   return out;
 }
 
-std::vector<int> y_row_tasks(const IndexMaps& m, int workers, int* cap) {
-  std::vector<std::pair<double, int>> items;
+YPlan y_plan(const IndexMaps& m, const std::vector<double>& cprime) {
+  YPlan p;
+  std::vector<int> cwoff(m.tuples.size());
+  for (std::size_t q = 0; q < m.tuples.size(); ++q) {
+    const Tuple& tp = m.tuples[q];
+    const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+    cwoff[q] = static_cast<int>(p.cw.size());
+    for (int a2 = 0; a2 <= tp.j2; ++a2)
+      for (int ma = 0; ma <= tp.j; ++ma) {
+        const int a1 = ma + D - a2;
+        double c = 0.0;
+        if (a1 >= 0 && a1 <= tp.j1) c = cprime[tp.cg_off + a1 * (tp.j2 + 1) + a2];
+        p.cw.push_back(c);
+      }
+  }
   for (int j = 0; j <= m.T; ++j)
-    for (int mb = 0; 2 * mb <= j; ++mb) items.push_back({y_row_cost(m, j, mb), j * 64 + mb});
+    for (int mb = 0; 2 * mb <= j; ++mb) {
+      p.row_begin.push_back(static_cast<int>(p.items.size()));
+      const int L = (2 * mb == j) ? j / 2 + 1 : j + 1;
+      double cost = 0.0;
+      for (std::size_t q = 0; q < m.tuples.size(); ++q) {
+        const Tuple& tp = m.tuples[q];
+        if (tp.j != j) continue;
+        const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+        const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
+        for (int mb1 = lo; mb1 <= hi; ++mb1) {
+          const int mb2 = mb + D - mb1;
+          const bool m1 = 2 * mb1 > tp.j1, m2 = 2 * mb2 > tp.j2;
+          const int r1 = m1 ? tp.j1 - mb1 : mb1, r2 = m2 ? tp.j2 - mb2 : mb2;
+          const int x = m.half_off[tp.j1] + r1 * (tp.j1 + 1);
+          const int y = m.half_off[tp.j2] + r2 * (tp.j2 + 1);
+          const int z = tp.j1 | (tp.j2 << 8) | (D << 16) | ((m1 ? 1 : 0) << 24) |
+                        ((m2 ? 1 : 0) << 25) | ((j + 1) << 26);
+          p.items.push_back({x, y, z, cwoff[q]});
+          cost += (tp.j2 + 1) * (6.0 * L + 12.0) + 4.0 * L + 20.0;
+        }
+      }
+      p.row_cost.push_back(cost);
+    }
+  p.row_begin.push_back(static_cast<int>(p.items.size()));
+  return p;
+}
+
+std::vector<double> y_item_weights(const IndexMaps& m, const std::vector<double>& wtab) {
+  std::vector<double> out;
+  for (int j = 0; j <= m.T; ++j)
+    for (int mb = 0; 2 * mb <= j; ++mb)
+      for (const Tuple& tp : m.tuples) {
+        if (tp.j != j) continue;
+        const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+        const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
+        for (int mb1 = lo; mb1 <= hi; ++mb1)
+          out.push_back(wtab[tp.cg_off + mb1 * (tp.j2 + 1) + (mb + D - mb1)]);
+      }
+  return out;
+}
+
+YCoopPlan ycoop_plan(const IndexMaps& m, int warps) {
+  YCoopPlan p;
+  p.warps = warps;
+  for (int j = 0; j <= m.T; ++j)
+    for (int mb = 0; 2 * mb <= j; ++mb) {
+      std::vector<std::pair<double, int>> costs;
+      std::vector<std::array<int, 4>> its;
+      int local = -1;  // index of the tuple among those targeting j
+      for (std::size_t q = 0; q < m.tuples.size(); ++q) {
+        const Tuple& tp = m.tuples[q];
+        if (tp.j != j) continue;
+        ++local;
+        const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+        int macs = 0;
+        for (int ma = 0; ma <= j; ++ma)
+          macs += std::max(0, std::min(tp.j1, ma + D) - std::max(0, ma + D - tp.j2) + 1);
+        const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
+        for (int mb1 = lo; mb1 <= hi; ++mb1) {
+          costs.push_back({6.0 * macs + 2.0 * (j + 1) + 4.0 * (tp.j1 + tp.j2 + 2) + 20.0,
+                           static_cast<int>(its.size())});
+          its.push_back({static_cast<int>(q), mb1, mb + D - mb1, local});
+        }
+      }
+      double tot = 0.0;
+      for (auto& c : costs) tot += c.first;
+      p.row_cost.push_back(tot);
+      auto buckets = lpt(costs, warps);
+      const int base = static_cast<int>(p.items.size());
+      int off = base;
+      for (int w = 0; w < warps; ++w) {
+        // same tuple order in every warp: consecutive items reuse one body
+        std::sort(buckets[w].begin(), buckets[w].end(), [&](int x, int y) {
+          return its[x][3] != its[y][3] ? its[x][3] < its[y][3] : its[x][1] < its[y][1];
+        });
+        p.rw_begin.push_back(off);
+        for (int idx : buckets[w]) p.items.push_back(its[idx]);
+        off = static_cast<int>(p.items.size());
+      }
+      p.rw_begin.push_back(off);
+    }
+  return p;
+}
+
+std::vector<double> ycoop_weights(const YCoopPlan& p, const IndexMaps& m,
+                                  const std::vector<double>& wtab) {
+  std::vector<double> out(p.items.size());
+  for (std::size_t i = 0; i < p.items.size(); ++i) {
+    const Tuple& tp = m.tuples[p.items[i][0]];
+    out[i] = wtab[tp.cg_off + p.items[i][1] * (tp.j2 + 1) + p.items[i][2]];
+  }
+  return out;
+}
+
+std::vector<int> y_row_schedule(const IndexMaps& m, const std::vector<double>& row_cost,
+                                int workers, int* cap) {
+  std::vector<std::pair<double, int>> items;
+  int rid = 0;
+  for (int j = 0; j <= m.T; ++j)
+    for (int mb = 0; 2 * mb <= j; ++mb, ++rid) items.push_back({row_cost[rid], j * 64 + mb});
   auto buckets = lpt(items, workers);
   int c = 0;
   for (auto& b : buckets) c = std::max<int>(c, static_cast<int>(b.size()));
@@ -247,42 +344,6 @@ std::vector<int> y_row_tasks(const IndexMaps& m, int workers, int* cap) {
     for (std::size_t k = 0; k < buckets[w].size(); ++k) out[w * c + k] = buckets[w][k];
   *cap = c;
   return out;
-}
-
-GenericYPlan generic_y_plan(const IndexMaps& m, int workers) {
-  GenericYPlan p;
-  std::vector<std::pair<double, int>> items;
-  for (int j = 0; j <= m.T; ++j)
-    for (int mb = 0; 2 * mb <= j; ++mb)
-      for (int ma = 0; ma <= j; ++ma) {
-        if (2 * mb == j && 2 * ma > j) continue;  // never read: zero weight
-        const int id = static_cast<int>(p.elem_info.size() / 6);
-        const int begin = static_cast<int>(p.elem_tups.size());
-        double cost = 0.0;
-        for (std::size_t q = 0; q < m.tuples.size(); ++q) {
-          const Tuple& tp = m.tuples[q];
-          if (tp.j != j) continue;
-          const int D = (tp.j1 + tp.j2 - tp.j) / 2;
-          const int nb = std::min(tp.j1, mb + D) - std::max(0, mb + D - tp.j2) + 1;
-          const int na = std::min(tp.j1, ma + D) - std::max(0, ma + D - tp.j2) + 1;
-          if (nb <= 0 || na <= 0) continue;
-          p.elem_tups.push_back(static_cast<int>(q));
-          cost += nb * (na * 10.0 + 8.0);
-        }
-        const int hidx = m.half_off[j] + mb * (j + 1) + ma;
-        p.elem_info.insert(p.elem_info.end(),
-                           {j, mb, ma, hidx, begin, static_cast<int>(p.elem_tups.size())});
-        items.push_back({cost, id});
-      }
-  auto buckets = lpt(items, workers);
-  int c = 0;
-  for (auto& b : buckets) c = std::max<int>(c, static_cast<int>(b.size()));
-  c += 1;
-  p.cap = c;
-  p.elem_tasks.assign(static_cast<std::size_t>(workers) * c, -1);
-  for (int w = 0; w < workers; ++w)
-    for (std::size_t k = 0; k < buckets[w].size(); ++k) p.elem_tasks[w * c + k] = buckets[w][k];
-  return p;
 }
 
 // ---------------------------------------------------------------------------

@@ -55,8 +55,10 @@ double f_scale(int t, int mb, int ma);  // g*h
 std::vector<double> cprime_table(const IndexMaps& m, const std::vector<double>& cg);
 // W(tuple; mb1, mb2) = fold_beta * cg / (G(j1,mb1) G(j2,mb2) g(j, mb)),
 // G(t,m) = g(t, min(m, t-m)); zero where the target row is not stored.
+// With mirror_signs, the (-1)^mb factor of mirrored factor rows is folded in
+// (the kernel then applies only (-1)^ma and the conjugation).
 std::vector<double> w_table(const IndexMaps& m, const std::vector<double>& cg,
-                            const double* beta);
+                            const double* beta, bool mirror_signs);
 
 // Per-half-index scale 1/f (u = v/f) and f, in half index order.
 std::vector<double> half_f(const IndexMaps& m);
@@ -69,21 +71,37 @@ std::vector<double> half_ywgt(const IndexMaps& m);
 // as src*4 + (mirrored?2:0) + (negative?1:0).
 std::vector<int> full_expand_map(const IndexMaps& m);
 
-// compute_Y work decomposition: target rows (j, mb), with a cost model
-// (complex MACs weighted by instruction counts), assigned to `workers`
-// buckets by longest-processing-time.  Returns per-worker lists packed as
-// [worker][k] = j*64 + mb, terminated by -1, each worker padded to `cap`.
-std::vector<int> y_row_tasks(const IndexMaps& m, int workers, int* cap);
 
-// Generic compute_Y (any T): Y target elements (j, mb, ma) with the tuples
-// feeding them; packed int records consumed by the generic kernel.
-struct GenericYPlan {
-  std::vector<int> elem_tasks;  // per worker lists of target element ids, -1 terminated
-  int cap = 0;
-  std::vector<int> elem_info;   // per target element: j, mb, ma, hidx, tup_begin, tup_end
-  std::vector<int> elem_tups;   // tuple ids
+// compute_Y row-pair items (sliding-window kernel, kernels.cuh k_compute_Y).
+// Target rows (j, mb <= j/2) are numbered rid = sum_{s<j}(s/2+1) + mb; row
+// rid owns items [row_begin[rid], row_begin[rid+1]), one per contributing
+// (tuple, mb1).  Item: x = half-storage start of factor row mb1 of level j1
+// (or of its mirror source), y = same for row mb2 of level j2, z = packed
+// j1 | j2<<8 | D<<16 | mirrored1<<24 | mirrored2<<25 | (j+1)<<26, w = offset
+// of the tuple's windowed coefficient block.  itw = W' (beta-dependent).
+struct YPlan {
+  std::vector<std::array<int, 4>> items;
+  std::vector<int> row_begin;
+  std::vector<double> cw;       // windowed C': per tuple (j2+1) x (j+1)
+  std::vector<double> row_cost; // per row (FP64 instructions, for scheduling)
 };
-GenericYPlan generic_y_plan(const IndexMaps& m, int workers);
+YPlan y_plan(const IndexMaps& m, const std::vector<double>& cprime);
+std::vector<double> y_item_weights(const IndexMaps& m, const std::vector<double>& wtab);
+// Unrolled cooperative compute_Y (2J <= 8): per target row, the row-pair
+// items {tuple q, mb1, mb2} are LPT-split over `warps` warps; items of row
+// rid, warp w live in [rw_begin[rid*(warps+1)+w], rw_begin[rid*(warps+1)+w+1]).
+struct YCoopPlan {
+  int warps = 0;
+  std::vector<std::array<int, 4>> items;
+  std::vector<int> rw_begin;
+  std::vector<double> row_cost;
+};
+YCoopPlan ycoop_plan(const IndexMaps& m, int warps);
+std::vector<double> ycoop_weights(const YCoopPlan& p, const IndexMaps& m,
+                                  const std::vector<double>& wtab);
+// LPT assignment of rows to workers: [worker][cap] row codes j*64+mb, -1 end.
+std::vector<int> y_row_schedule(const IndexMaps& m, const std::vector<double>& row_cost,
+                                int workers, int* cap);
 
 // Reference-order neighbor list builder (harness.hpp:119-202, orthorhombic).
 // Returns max neighbor count or -1 (err set).

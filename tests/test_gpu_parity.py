@@ -190,8 +190,8 @@ def test_stage_timing_and_tuning_knobs(snap):
     base = snap.run_pipeline(p)
     eng = snap.SnapEngine.for_problem(p)
     eng.set_problem(p)
-    for yw, yp in [(4, 1), (8, 2), (12, 3), (16, 1)]:
-        eng.tune(y_warps=yw, y_parts=yp)
+    for yw, yp, ta in [(4, 1, 0), (8, 2, 32), (6, 3, 16), (8, 1, 8), (2, 0, 0)]:
+        eng.tune(y_warps=yw, y_parts=yp, y_tile_atoms=ta)
         eng.enable_stage_timing(True)
         eng.run()
         st = eng.stage_times()

@@ -1,7 +1,6 @@
 """Quick device timing of the force step (development helper)."""
 import sys, time
 import numpy as np
-import torch
 sys.path.insert(0, '.')
 import paper_2011_12875_b200 as snap
 
@@ -19,20 +18,16 @@ def run(nx, ny, nz, T=8, reps=10, tune=None):
     med = {k: float(np.median(v)) for k, v in st.items()}
     eng.enable_stage_timing(False)
     eng.run(); eng.synchronize()
-    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(reps): eng.run()
     eng.synchronize()
     dt = (time.perf_counter() - t0) / reps * 1e3
     n = p.natoms
-    print(f"T={T} N={n} tune={tune} stages(ms)={ {k: round(v,4) for k,v in med.items()} } graph step {dt:.4f} ms -> {n/dt:.1f} Katom-steps/s, {dt*1e3/n*1e3:.2f} ns/atom", flush=True)
+    print(f"T={T} N={n} tune={tune} stages(ms)={ {k: round(v,4) for k,v in med.items()} } step {dt:.4f} ms -> {n/dt:.1f} Katom-steps/s, {dt*1e6/n:.2f} ns/atom", flush=True)
     eng.close()
 
 if __name__ == "__main__":
-    run(10, 10, 10)
-    run(64, 64, 32, reps=5)
-    for tn in [(4,1,0),(8,1,0),(12,1,0),(16,1,0)]:
-        run(64, 64, 32, reps=3, tune=tn)
-    run(10,10,10, tune=(8,1,0)); run(10,10,10, tune=(8,2,0)); run(10,10,10, tune=(16,1,0))
-    run(32, 32, 16, T=14, reps=2)
+    for spec in sys.argv[1:]:
+        f = [int(x) for x in spec.split(",")]
+        tune = tuple(f[4:7]) if len(f) > 4 else None
+        run(f[0], f[1], f[2], T=f[3], reps=10 if f[0]*f[1]*f[2] < 50000 else 3, tune=tune)
