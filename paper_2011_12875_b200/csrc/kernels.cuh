@@ -652,7 +652,7 @@ __host__ __device__ constexpr int c_n_tuples(int T) {
 }
 // Band limits with an unrolled compute_Y; their C' tables are stacked in
 // constant memory (2J = 7 is left to the windowed kernel to stay < 64 KB).
-__host__ __device__ constexpr bool y_unrolled(int T) { return T <= 8 && T != 7; }
+__host__ __device__ constexpr bool y_unrolled(int T) { return T == 8; }
 __host__ __device__ constexpr int cp_base(int T) {
   int o = 0;
   for (int s = 0; s < T; ++s)
@@ -661,6 +661,25 @@ __host__ __device__ constexpr int cp_base(int T) {
 }
 constexpr int kCpTotal = cp_base(9);
 __constant__ double cCP[kCpTotal];
+
+// ---------------------------------------------------------------------------
+// compute_Y, constant-window variant (2J <= 8): the sliding-window loop of
+// k_compute_Y over the FULL mirrored X tile (zero-padded: no mirror logic,
+// no index clamps) with the windowed C' coefficients in constant memory at
+// warp-uniform offsets and W folded into the x2 element.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr bool y_cwin(int T) { return T <= 8; }
+__host__ __device__ constexpr int c_cw_total(int T) {
+  int o = 0;
+  for (int j1 = 0; j1 <= T; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) o += (j2 + 1) * (j + 1);
+  return o;
+}
+__host__ __device__ constexpr int cw_base(int T) { return T == 8 ? 0 : -1; }
+constexpr int kCwTotal = c_cw_total(8);
+__constant__ double cCW[kCwTotal];
+constexpr int kXPad = 16;  // zero elements before/after each X plane
 
 struct YCArgs {
   const double* V;      // [tile32][2][NH][32]
@@ -676,7 +695,11 @@ struct YCArgs {
   EnergyOut E;
 };
 
-template <int T, int J1, int J2, int J>
+// One row-pair item of tuple (J1, J2) -> J: a1-major so consecutive MACs hit
+// different accumulators (ILP), W folded into the x1 element, outputs
+// ma <= NOUT-1 only (NOUT = J/2+1 on the middle row, whose upper half is
+// never read; J+1 otherwise).
+template <int T, int J1, int J2, int J, int NOUT>
 __device__ __forceinline__ void yc_item(const double* __restrict__ sX, int lane, int mb1,
                                         int mb2, double w, double (&accr)[J + 1],
                                         double (&acci)[J + 1]) {
@@ -685,32 +708,27 @@ __device__ __forceinline__ void yc_item(const double* __restrict__ sX, int lane,
   constexpr int CB = cp_base(T) + c_cg_off(T, J1, J2, J);
   const double* p1 = sX + (c_full_off(J1) + mb1 * (J1 + 1)) * 32 + lane;
   const double* p2 = sX + (c_full_off(J2) + mb2 * (J2 + 1)) * 32 + lane;
-  double x1r[J1 + 1], x1i[J1 + 1], x2r[J2 + 1], x2i[J2 + 1];
-#pragma unroll
-  for (int a = 0; a <= J1; ++a) {
-    x1r[a] = p1[a * 32];
-    x1i[a] = p1[(NF + a) * 32];
-  }
+  double x2r[J2 + 1], x2i[J2 + 1];
 #pragma unroll
   for (int a = 0; a <= J2; ++a) {
     x2r[a] = p2[a * 32];
     x2i[a] = p2[(NF + a) * 32];
   }
 #pragma unroll
-  for (int ma = 0; ma <= J; ++ma) {
-    const int alo = cmax(0, ma + D - J2), ahi = cmin(J1, ma + D);
-    double sr = 0.0, si = 0.0;
+  for (int a1 = 0; a1 <= J1; ++a1) {
+    // valid partners: ma = a1 + a2 - D in [0, NOUT-1], a2 in [0, J2]
+    const int a2lo = cmax(0, D - a1), a2hi = cmin(J2, NOUT - 1 + D - a1);
+    if (a2lo > a2hi) continue;
+    const double yr = w * p1[a1 * 32], yi = w * p1[(NF + a1) * 32];
 #pragma unroll
-    for (int a1 = alo; a1 <= ahi; ++a1) {
-      const int a2 = ma + D - a1;
+    for (int a2 = a2lo; a2 <= a2hi; ++a2) {
+      const int ma = a1 + a2 - D;
       const double cc = cCP[CB + a1 * (J2 + 1) + a2];
-      const double tr = x1r[a1] * x2r[a2] - x1i[a1] * x2i[a2];
-      const double ti = x1r[a1] * x2i[a2] + x1i[a1] * x2r[a2];
-      sr = fma(cc, tr, sr);
-      si = fma(cc, ti, si);
+      const double tr = yr * x2r[a2] - yi * x2i[a2];
+      const double ti = yr * x2i[a2] + yi * x2r[a2];
+      accr[ma] = fma(cc, tr, accr[ma]);
+      acci[ma] = fma(cc, ti, acci[ma]);
     }
-    accr[ma] = fma(w, sr, accr[ma]);
-    acci[ma] = fma(w, si, acci[ma]);
   }
 }
 
@@ -736,14 +754,14 @@ __host__ __device__ constexpr int c_ntuples_for_j(int T, int J) {
 
 // dispatch an item of target row J to its tuple body through one dense
 // switch (a single indirect branch) on the item's local tuple index
-template <int T, int J>
+template <int T, int J, int NOUT>
 __device__ __forceinline__ void yc_dispatch(int ql, const double* sX, int lane, int mb1, int mb2,
                                             double w, double (&ar)[J + 1], double (&ai)[J + 1]) {
-#define YCASE(L)                                                                               \
-  case L:                                                                                      \
-    if constexpr (L < c_ntuples_for_j(T, J))                                                   \
-      yc_item<T, c_tuple_for_j(T, J, L, 0), c_tuple_for_j(T, J, L, 1), J>(sX, lane, mb1, mb2, \
-                                                                          w, ar, ai);          \
+#define YCASE(L)                                                                     \
+  case L:                                                                            \
+    if constexpr (L < c_ntuples_for_j(T, J))                                         \
+      yc_item<T, c_tuple_for_j(T, J, L, 0), c_tuple_for_j(T, J, L, 1), J, NOUT>(     \
+          sX, lane, mb1, mb2, w, ar, ai);                                            \
     break;
   switch (ql) {
     YCASE(0) YCASE(1) YCASE(2) YCASE(3) YCASE(4) YCASE(5) YCASE(6) YCASE(7) YCASE(8) YCASE(9)
@@ -754,10 +772,11 @@ __device__ __forceinline__ void yc_dispatch(int ql, const double* sX, int lane, 
 #undef YCASE
 }
 
-template <int T, int J>
+template <int T, int J, bool MID>
 __device__ __forceinline__ void yc_row(const double* __restrict__ sX, double* __restrict__ sred,
                                        int lane, int w, int nw, int mb, int rid, const YCArgs& A,
                                        double* __restrict__ Yt, double& e_acc) {
+  constexpr int NOUT = MID ? J / 2 + 1 : J + 1;
   constexpr int NF = c_full_off(T + 1);
   constexpr int NH = c_half_off(T + 1);
   double ar[J + 1], ai[J + 1];
@@ -779,7 +798,7 @@ __device__ __forceinline__ void yc_row(const double* __restrict__ sX, double* __
       mn = __ldg(A.items + it + 1);
       wn = __ldg(A.itw + it + 1);
     }
-    yc_dispatch<T, J>(m.x, sX, lane, m.y, m.z, wt, ar, ai);
+    yc_dispatch<T, J, NOUT>(m.x, sX, lane, m.y, m.z, wt, ar, ai);
     m = mn;
     wt = wn;
   }
@@ -841,15 +860,167 @@ __global__ void __launch_bounds__(384, 1) k_compute_Y_unrolled(const YCArgs A) {
     if (code < 0) break;
     const int j = code >> 6, mb = code & 63;
     const int rid = c_acc_off(j) + mb;
-#define YCROW(JJ)                                                                 \
-  case JJ:                                                                        \
-    if constexpr (JJ <= T) yc_row<T, JJ>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc); \
+#define YCROW(JJ)                                                                       \
+  case JJ:                                                                              \
+    if constexpr (JJ <= T) {                                                            \
+      if (2 * mb == JJ) yc_row<T, JJ, true>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc); \
+      else yc_row<T, JJ, false>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc);          \
+    }                                                                                   \
     break;
     switch (j) {
       YCROW(0) YCROW(1) YCROW(2) YCROW(3) YCROW(4) YCROW(5) YCROW(6) YCROW(7) YCROW(8)
       default: break;
     }
 #undef YCROW
+  }
+  se[w][lane] = e_acc;
+  __syncthreads();
+  if (w == 0) {
+    double s = 0.0;
+    for (int q = 0; q < nw; ++q) s += se[q][lane];
+    const int atom = tile * 32 + lane;
+    energy_epilogue(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
+  }
+}
+
+struct YWArgs {
+  const double* V;
+  double* Y;
+  const int* expand;
+  const int4* items;    // {x1 window base (full idx + D), x2 row base, J2 | coff<<8, 0}
+  const double* itw;    // W per item
+  const int* rw_begin;  // [row][warp]
+  int nwarps;
+  const int* tasks;
+  int task_cap;
+  int nlocal;
+  EnergyOut E;
+};
+
+template <int T, int J, bool MID>
+__device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __restrict__ sred,
+                                       int lane, int w, int nw, int mb, int rid, const YWArgs& A,
+                                       double* __restrict__ Yt, double& e_acc) {
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int NP = NF + 2 * kXPad;  // padded plane length
+  constexpr int NH = c_half_off(T + 1);
+  constexpr int L = MID ? J / 2 + 1 : J + 1;
+  constexpr int JW = J + 1;
+  constexpr int CWB = cw_base(T);
+  double ar[L], ai[L];
+#pragma unroll
+  for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
+  const int* rb = A.rw_begin + rid * (A.nwarps + 1);
+  const int b = __ldg(rb + w), e = __ldg(rb + w + 1);
+  for (int it = b; it < e; ++it) {
+    const int4 m = __ldg(A.items + it);
+    const double wt = __ldg(A.itw + it);
+    const int J2 = m.z & 0xff;
+    const int coff = CWB + (m.z >> 8);
+    const double* p1 = sX + (kXPad + m.x) * 32 + lane;  // x1[m.x + k] at p1[k*32]
+    const double* p2 = sX + (kXPad + m.y) * 32 + lane;
+    double wr[L], wi[L];
+#pragma unroll
+    for (int ma = 0; ma < L; ++ma) {
+      wr[ma] = p1[ma * 32];
+      wi[ma] = p1[(NP + ma) * 32];
+    }
+    for (int a2 = 0; a2 <= J2; ++a2) {
+      const double x2r = wt * p2[a2 * 32], x2i = wt * p2[(NP + a2) * 32];
+      const double* c = cCW + coff + a2 * JW;
+#pragma unroll
+      for (int ma = 0; ma < L; ++ma) {
+        const double cc = c[ma];
+        const double pr = wr[ma] * x2r - wi[ma] * x2i;
+        const double pi = wr[ma] * x2i + wi[ma] * x2r;
+        ar[ma] = fma(cc, pr, ar[ma]);
+        ai[ma] = fma(cc, pi, ai[ma]);
+      }
+#pragma unroll
+      for (int ma = L - 1; ma > 0; --ma) {
+        wr[ma] = wr[ma - 1];
+        wi[ma] = wi[ma - 1];
+      }
+      wr[0] = p1[(-a2 - 1) * 32];
+      wi[0] = p1[(NP - a2 - 1) * 32];
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    sred[((w * (T + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
+    sred[((w * (T + 1) + m) * 2 + 1) * 32 + lane] = ai[m];
+  }
+  __syncthreads();
+  const int hb = c_half_off(J) + mb * (J + 1);
+  const int fb = kXPad + c_full_off(J) + mb * (J + 1);
+  for (int ma = w; ma <= J; ma += nw) {
+    double yr = 0.0, yi = 0.0;
+    if (ma < L) {
+      for (int q = 0; q < nw; ++q) {
+        yr += sred[((q * (T + 1) + ma) * 2 + 0) * 32 + lane];
+        yi += sred[((q * (T + 1) + ma) * 2 + 1) * 32 + lane];
+      }
+      const double wgt = (MID && 2 * ma == J) ? 0.5 : 1.0;
+      yr *= wgt;
+      yi *= wgt;
+      e_acc += yr * sX[(fb + ma) * 32 + lane] + yi * sX[(NP + fb + ma) * 32 + lane];
+    }
+    Yt[(size_t)(hb + ma) * 32] = yr;
+    Yt[(size_t)(NH + hb + ma) * 32] = yi;
+  }
+  __syncthreads();
+}
+
+template <int T>
+__global__ void __launch_bounds__(384, 1) k_compute_Y_cwin(const YWArgs A) {
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int NP = NF + 2 * kXPad;
+  constexpr int NH = c_half_off(T + 1);
+  extern __shared__ double smem[];
+  double* sX = smem;                  // [re|im][pad | full idx | pad][32]
+  double* sred = smem + 2 * NP * 32;  // [warp][T+1][re|im][32]
+  __shared__ double se[12][32];
+  const int tile = blockIdx.x;
+  const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
+  for (int e = threadIdx.x; e < kXPad * 32; e += blockDim.x) {
+    sX[e] = sX[(kXPad + NF) * 32 + e] = 0.0;
+    sX[NP * 32 + e] = sX[(NP + kXPad + NF) * 32 + e] = 0.0;
+  }
+  for (int e = threadIdx.x; e < NF * 32; e += blockDim.x) {
+    const int f = e >> 5, ln = e & 31;
+    const int code = __ldg(A.expand + f);
+    const int src = code >> 2;
+    double re = Vt[src * 32 + ln], im = Vt[(NH + src) * 32 + ln];
+    if (code & 2) im = -im;
+    if (code & 1) {
+      re = -re;
+      im = -im;
+    }
+    sX[(kXPad + f) * 32 + ln] = re;
+    sX[(NP + kXPad + f) * 32 + ln] = im;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
+  double* Yt = A.Y + (size_t)tile * 2 * NH * 32 + lane;
+  double e_acc = 0.0;
+  for (int q = 0;; ++q) {
+    const int code = __ldg(tasks + q);
+    if (code < 0) break;
+    const int j = code >> 6, mb = code & 63;
+    const int rid = c_acc_off(j) + mb;
+#define YWROW(JJ)                                                                       \
+  case JJ:                                                                              \
+    if constexpr (JJ <= T) {                                                            \
+      if (2 * mb == JJ) yw_row<T, JJ, true>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc); \
+      else yw_row<T, JJ, false>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc);          \
+    }                                                                                   \
+    break;
+    switch (j) {
+      YWROW(0) YWROW(1) YWROW(2) YWROW(3) YWROW(4) YWROW(5) YWROW(6) YWROW(7) YWROW(8)
+      default: break;
+    }
+#undef YWROW
   }
   se[w][lane] = e_acc;
   __syncthreads();

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -86,6 +87,8 @@ struct snapgpu_ctx {
   DevBuf<int> d_rowbeg, d_tasks, d_expand, d_rwbeg;
   YPlan yplan;
   YCoopPlan ycplan;
+  int y_impl = 0;  // 2J<=8: 0 constant-window, 1 unrolled, 2 half-V window
+  DevBuf<int4> d_witems;
   int task_cap = 0;
   int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
   int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
@@ -238,6 +241,31 @@ struct LaunchY {
   }
   static void go(snapgpu_ctx* c) {
     constexpr int NH = c_half_off(T + 1);
+    if constexpr (cw_base(T) >= 0) {
+      if (c->y_impl == 0) {
+        constexpr int NF = c_full_off(T + 1);
+        constexpr int NP = NF + 2 * kXPad;
+        YWArgs a;
+        a.V = c->d_V.p;
+        a.Y = c->d_Y.p;
+        a.expand = c->d_expand.p;
+        a.items = c->d_witems.p;
+        a.itw = c->d_citw.p;
+        a.rw_begin = c->d_rwbeg.p;
+        a.nwarps = c->ycplan.warps;
+        a.tasks = c->d_tasks.p;
+        a.task_cap = c->task_cap;
+        a.nlocal = c->nlocal;
+        a.E = energy_out(c);
+        const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)c->y_warps * (T + 1) * 2 * 32);
+        CK(cudaFuncSetAttribute(k_compute_Y_cwin<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        dim3 grid(c->ntiles, c->y_parts_used);
+        k_compute_Y_cwin<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+        CK(cudaGetLastError());
+        return;
+      }
+    }
     if constexpr (y_unrolled(T)) {
       constexpr int NF = c_full_off(T + 1);
       YCArgs a;
@@ -299,7 +327,7 @@ void build_ycoop(snapgpu_ctx* c);
 void plan_y(snapgpu_ctx* c) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  if (y_unrolled(c->T)) {  // one 32-atom tile per CTA, all warps per row
+  if (c->y_impl <= 1) {  // one 32-atom tile per CTA, all warps per row
     if (c->ycplan.warps != c->y_warps) build_ycoop(c);
     int parts = c->y_parts;
     // one CTA per SM: never exceed a single wave
@@ -325,7 +353,7 @@ void plan_y(snapgpu_ctx* c) {
 }
 
 void upload_beta(snapgpu_ctx* c) {
-  if (y_unrolled(c->T)) {
+  if (c->y_impl <= 1) {
     const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
     const std::vector<double> itw = ycoop_weights(c->ycplan, c->maps, W);
     c->d_citw.alloc(std::max<size_t>(1, itw.size()));
@@ -346,10 +374,40 @@ void build_ycoop(snapgpu_ctx* c) {
     it[q] = make_int4(c->ycplan.items[q][3], c->ycplan.items[q][1], c->ycplan.items[q][2], 0);
   c->d_citems.alloc(std::max<size_t>(1, it.size()));
   CK(cudaMemcpy(c->d_citems.p, it.data(), it.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  if (c->y_impl == 0) {  // constant-window items
+    std::vector<int> cwoff(c->maps.tuples.size());
+    int o = 0;
+    for (size_t q = 0; q < cwoff.size(); ++q) {
+      cwoff[q] = o;
+      o += (c->maps.tuples[q].j2 + 1) * (c->maps.tuples[q].j + 1);
+    }
+    std::vector<int4> wi(c->ycplan.items.size());
+    for (size_t q = 0; q < wi.size(); ++q) {
+      const Tuple& tp = c->maps.tuples[c->ycplan.items[q][0]];
+      const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+      const int mb1 = c->ycplan.items[q][1], mb2 = c->ycplan.items[q][2];
+      wi[q] = make_int4(c->maps.full_off[tp.j1] + mb1 * (tp.j1 + 1) + D,
+                        c->maps.full_off[tp.j2] + mb2 * (tp.j2 + 1),
+                        tp.j2 | (cwoff[c->ycplan.items[q][0]] << 8), 0);
+    }
+    c->d_witems.alloc(std::max<size_t>(1, wi.size()));
+    CK(cudaMemcpy(c->d_witems.p, wi.data(), wi.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  }
   c->d_rwbeg.alloc(c->ycplan.rw_begin.size());
   CK(cudaMemcpy(c->d_rwbeg.p, c->ycplan.rw_begin.data(), c->ycplan.rw_begin.size() * sizeof(int),
                 cudaMemcpyHostToDevice));
   upload_beta(c);
+}
+
+void upload_cwin(int device, int T, const YPlan& p) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == device && d.second == T) return;
+  CK(cudaMemcpyToSymbol(cCW, p.cw.data(), p.cw.size() * sizeof(double),
+                        static_cast<size_t>(cw_base(T)) * sizeof(double)));
+  done.push_back({device, T});
 }
 
 void upload_cprime(int device, int T, const IndexMaps& m, const std::vector<double>& cg) {
@@ -575,10 +633,21 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     up(c->d_items, it);
     up(c->d_rowbeg, c->yplan.row_begin);
     up(c->d_cw, c->yplan.cw);
-    if (y_unrolled(twojmax)) {
+    // compute_Y implementation: constant-window (default for 2J <= 8, where
+    // the windowed C' fits constant memory), unrolled (2J = 8), half-V window.
+    c->y_impl = 2;
+    if (cw_base(twojmax) >= 0) c->y_impl = 0;
+    if (const char* e = std::getenv("SNAPGPU_Y_IMPL")) {
+      const std::string v(e);
+      if (v == "unrolled" && y_unrolled(twojmax)) c->y_impl = 1;
+      if (v == "window") c->y_impl = 2;
+      if (v == "cwin" && cw_base(twojmax) >= 0) c->y_impl = 0;
+    }
+    if (c->y_impl <= 1) {
       c->y_warps = 12;
       up(c->d_expand, full_expand_map(c->maps));
-      upload_cprime(device, twojmax, c->maps, c->cg);
+      if (c->y_impl == 1) upload_cprime(device, twojmax, c->maps, c->cg);
+      else upload_cwin(device, twojmax, c->yplan);
       build_ycoop(c);  // uploads the beta-dependent item weights
     } else {
       upload_beta(c);
@@ -612,6 +681,7 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_citw.release();
   c->d_expand.release();
   c->d_rwbeg.release();
+  c->d_witems.release();
   c->d_tasks.release();
   c->d_numneigh.release();
   c->d_nbr.release();
@@ -927,7 +997,7 @@ int snapgpu_stage_times(snapgpu_ctx* c, float* out4) {
 int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int y_tile_atoms) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    require(y_warps >= 0 && y_warps <= (y_unrolled(c->T) ? 12 : 8),
+    require(y_warps >= 0 && y_warps <= (c->y_impl <= 1 ? 12 : 8),
             "tune: y_warps in [0,12] (2J <= 8) or [0,8]");
     require(y_tile_atoms == 0 || y_tile_atoms == 8 || y_tile_atoms == 16 || y_tile_atoms == 32,
             "tune: y_tile_atoms in {0, 8, 16, 32}");

@@ -290,11 +290,12 @@ YCoopPlan ycoop_plan(const IndexMaps& m, int warps) {
         ++local;
         const int D = (tp.j1 + tp.j2 - tp.j) / 2;
         int macs = 0;
-        for (int ma = 0; ma <= j; ++ma)
+        const int nout = (2 * mb == j) ? j / 2 + 1 : j + 1;
+        for (int ma = 0; ma < nout; ++ma)
           macs += std::max(0, std::min(tp.j1, ma + D) - std::max(0, ma + D - tp.j2) + 1);
         const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
         for (int mb1 = lo; mb1 <= hi; ++mb1) {
-          costs.push_back({6.0 * macs + 2.0 * (j + 1) + 4.0 * (tp.j1 + tp.j2 + 2) + 20.0,
+          costs.push_back({6.0 * macs + 2.0 * (tp.j1 + 1) + 4.0 * (tp.j1 + tp.j2 + 2) + 20.0,
                            static_cast<int>(its.size())});
           its.push_back({static_cast<int>(q), mb1, mb + D - mb1, local});
         }
@@ -302,14 +303,14 @@ YCoopPlan ycoop_plan(const IndexMaps& m, int warps) {
       double tot = 0.0;
       for (auto& c : costs) tot += c.first;
       p.row_cost.push_back(tot);
-      auto buckets = lpt(costs, warps);
+      // Items are enumerated tuple by tuple; dealing them round-robin keeps
+      // every warp on the same tuple body at the same time (instruction
+      // cache locality), with per-warp counts within one of each other.
+      std::vector<std::vector<int>> buckets(warps);
+      for (std::size_t i = 0; i < its.size(); ++i) buckets[i % warps].push_back(static_cast<int>(i));
       const int base = static_cast<int>(p.items.size());
       int off = base;
       for (int w = 0; w < warps; ++w) {
-        // same tuple order in every warp: consecutive items reuse one body
-        std::sort(buckets[w].begin(), buckets[w].end(), [&](int x, int y) {
-          return its[x][3] != its[y][3] ? its[x][3] < its[y][3] : its[x][1] < its[y][1];
-        });
         p.rw_begin.push_back(off);
         for (int idx : buckets[w]) p.items.push_back(its[idx]);
         off = static_cast<int>(p.items.size());
