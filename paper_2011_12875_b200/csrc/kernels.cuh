@@ -622,53 +622,18 @@ __global__ void __launch_bounds__(256) k_compute_Y(const YArgs A) {
 }
 
 // ===========================================================================
-// compute_Y, unrolled cooperative variant for 2J <= 8 (snap_core.hpp:1085-1200)
+// compute_Y, constant-window cooperative variant (2J <= 8)
 //
-// The per-tuple (j1, j2) -> j contraction body is fully unrolled (operands in
-// registers, C' coefficients as uniform constant-bank loads: ~85% of the
-// instructions are DFMA/DMUL).  Instruction-cache locality comes from the
-// schedule: all warps of the CTA (one CTA per SM, one 32-atom tile) work on
-// the SAME target row (j, mb) at the same time, each on an LPT-balanced share
-// of the row's row-pair items, so the live code is only the bodies of the
-// tuples targeting j (<= 55 KB at 2J = 8) instead of all 125 (~400 KB).
-// Partial rows meet in shared memory; X is the tile's full mirrored stack.
+// CTA = one 32-atom tile (lane = atom), its FULL mirrored stack X in shared
+// memory (zero-padded: no mirror logic, no index clamps), 12 warps.  All
+// warps work on the same target row (j, mb): the row's row-pair items are
+// LPT-split over the warps; each item runs the sliding-window loop of
+// k_compute_Y with the windowed C' coefficients in constant memory at
+// warp-uniform offsets and W folded into x2; the window advances U = 3
+// steps per block with compile-time register indexing.  Partial rows meet
+// in shared memory; each warp finishes a stripe of outputs.  The code is a
+// handful of small loops, so the SM's instruction caches hold it.
 // ===========================================================================
-__host__ __device__ constexpr int c_tuple_field(int T, int Q, int f) {
-  int n = 0;
-  for (int j1 = 0; j1 <= T; ++j1)
-    for (int j2 = 0; j2 <= j1; ++j2)
-      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) {
-        if (n == Q) return f == 0 ? j1 : (f == 1 ? j2 : j);
-        ++n;
-      }
-  return -1;
-}
-__host__ __device__ constexpr int c_n_tuples(int T) {
-  int n = 0;
-  for (int j1 = 0; j1 <= T; ++j1)
-    for (int j2 = 0; j2 <= j1; ++j2)
-      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) ++n;
-  return n;
-}
-// Band limits with an unrolled compute_Y; their C' tables are stacked in
-// constant memory (2J = 7 is left to the windowed kernel to stay < 64 KB).
-__host__ __device__ constexpr bool y_unrolled(int T) { return T == 8; }
-__host__ __device__ constexpr int cp_base(int T) {
-  int o = 0;
-  for (int s = 0; s < T; ++s)
-    if (y_unrolled(s)) o += c_cg_total(s);
-  return o;
-}
-constexpr int kCpTotal = cp_base(9);
-__constant__ double cCP[kCpTotal];
-
-// ---------------------------------------------------------------------------
-// compute_Y, constant-window variant (2J <= 8): the sliding-window loop of
-// k_compute_Y over the FULL mirrored X tile (zero-padded: no mirror logic,
-// no index clamps) with the windowed C' coefficients in constant memory at
-// warp-uniform offsets and W folded into the x2 element.
-// ---------------------------------------------------------------------------
-__host__ __device__ constexpr bool y_cwin(int T) { return T <= 8; }
 __host__ __device__ constexpr int c_cw_total(int T) {
   int o = 0;
   for (int j1 = 0; j1 <= T; ++j1)
@@ -676,212 +641,15 @@ __host__ __device__ constexpr int c_cw_total(int T) {
       for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) o += (j2 + 1) * (j + 1);
   return o;
 }
-__host__ __device__ constexpr int cw_base(int T) { return T == 8 ? 0 : -1; }
-constexpr int kCwTotal = c_cw_total(8);
+__host__ __device__ constexpr int cw_base(int T) {  // windowed C' of 2J = 0..8 stacked
+  if (T > 8) return -1;
+  int o = 0;
+  for (int s = 0; s < T; ++s) o += c_cw_total(s);
+  return o;
+}
+constexpr int kCwTotal = cw_base(8) + c_cw_total(8);
 __constant__ double cCW[kCwTotal];
 constexpr int kXPad = 16;  // zero elements before/after each X plane
-
-struct YCArgs {
-  const double* V;      // [tile32][2][NH][32]
-  double* Y;            // [tile32][2][NH][32]
-  const int* expand;    // full idx -> half src code (mirror map)
-  const int4* items;    // {local tuple index within j, mb1, mb2, 0}, per (row, warp)
-  const double* itw;    // W per item
-  const int* rw_begin;  // [row][warp] -> item range start; [row][W] = end
-  int nwarps;           // warps the item split was made for
-  const int* tasks;     // [part][cap] row codes, -1 terminated
-  int task_cap;
-  int nlocal;
-  EnergyOut E;
-};
-
-// One row-pair item of tuple (J1, J2) -> J: a1-major so consecutive MACs hit
-// different accumulators (ILP), W folded into the x1 element, outputs
-// ma <= NOUT-1 only (NOUT = J/2+1 on the middle row, whose upper half is
-// never read; J+1 otherwise).
-template <int T, int J1, int J2, int J, int NOUT>
-__device__ __forceinline__ void yc_item(const double* __restrict__ sX, int lane, int mb1,
-                                        int mb2, double w, double (&accr)[J + 1],
-                                        double (&acci)[J + 1]) {
-  constexpr int NF = c_full_off(T + 1);
-  constexpr int D = (J1 + J2 - J) / 2;
-  constexpr int CB = cp_base(T) + c_cg_off(T, J1, J2, J);
-  const double* p1 = sX + (c_full_off(J1) + mb1 * (J1 + 1)) * 32 + lane;
-  const double* p2 = sX + (c_full_off(J2) + mb2 * (J2 + 1)) * 32 + lane;
-  double x2r[J2 + 1], x2i[J2 + 1];
-#pragma unroll
-  for (int a = 0; a <= J2; ++a) {
-    x2r[a] = p2[a * 32];
-    x2i[a] = p2[(NF + a) * 32];
-  }
-#pragma unroll
-  for (int a1 = 0; a1 <= J1; ++a1) {
-    // valid partners: ma = a1 + a2 - D in [0, NOUT-1], a2 in [0, J2]
-    const int a2lo = cmax(0, D - a1), a2hi = cmin(J2, NOUT - 1 + D - a1);
-    if (a2lo > a2hi) continue;
-    const double yr = w * p1[a1 * 32], yi = w * p1[(NF + a1) * 32];
-#pragma unroll
-    for (int a2 = a2lo; a2 <= a2hi; ++a2) {
-      const int ma = a1 + a2 - D;
-      const double cc = cCP[CB + a1 * (J2 + 1) + a2];
-      const double tr = yr * x2r[a2] - yi * x2i[a2];
-      const double ti = yr * x2i[a2] + yi * x2r[a2];
-      accr[ma] = fma(cc, tr, accr[ma]);
-      acci[ma] = fma(cc, ti, acci[ma]);
-    }
-  }
-}
-
-// L-th coupling tuple (in reference order) whose target is J: field 0/1 = j1/j2.
-__host__ __device__ constexpr int c_tuple_for_j(int T, int J, int L, int f) {
-  int n = 0;
-  for (int j1 = 0; j1 <= T; ++j1)
-    for (int j2 = 0; j2 <= j1; ++j2)
-      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2)
-        if (j == J) {
-          if (n == L) return f == 0 ? j1 : j2;
-          ++n;
-        }
-  return -1;
-}
-__host__ __device__ constexpr int c_ntuples_for_j(int T, int J) {
-  int n = 0;
-  for (int j1 = 0; j1 <= T; ++j1)
-    for (int j2 = 0; j2 <= j1; ++j2)
-      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) n += (j == J);
-  return n;
-}
-
-// dispatch an item of target row J to its tuple body through one dense
-// switch (a single indirect branch) on the item's local tuple index
-template <int T, int J, int NOUT>
-__device__ __forceinline__ void yc_dispatch(int ql, const double* sX, int lane, int mb1, int mb2,
-                                            double w, double (&ar)[J + 1], double (&ai)[J + 1]) {
-#define YCASE(L)                                                                     \
-  case L:                                                                            \
-    if constexpr (L < c_ntuples_for_j(T, J))                                         \
-      yc_item<T, c_tuple_for_j(T, J, L, 0), c_tuple_for_j(T, J, L, 1), J, NOUT>(     \
-          sX, lane, mb1, mb2, w, ar, ai);                                            \
-    break;
-  switch (ql) {
-    YCASE(0) YCASE(1) YCASE(2) YCASE(3) YCASE(4) YCASE(5) YCASE(6) YCASE(7) YCASE(8) YCASE(9)
-    YCASE(10) YCASE(11) YCASE(12) YCASE(13) YCASE(14) YCASE(15) YCASE(16) YCASE(17) YCASE(18)
-    YCASE(19) YCASE(20) YCASE(21) YCASE(22) YCASE(23) YCASE(24)
-    default: break;
-  }
-#undef YCASE
-}
-
-template <int T, int J, bool MID>
-__device__ __forceinline__ void yc_row(const double* __restrict__ sX, double* __restrict__ sred,
-                                       int lane, int w, int nw, int mb, int rid, const YCArgs& A,
-                                       double* __restrict__ Yt, double& e_acc) {
-  constexpr int NOUT = MID ? J / 2 + 1 : J + 1;
-  constexpr int NF = c_full_off(T + 1);
-  constexpr int NH = c_half_off(T + 1);
-  double ar[J + 1], ai[J + 1];
-#pragma unroll
-  for (int m = 0; m <= J; ++m) ar[m] = ai[m] = 0.0;
-  const int* rb = A.rw_begin + rid * (A.nwarps + 1);
-  const int b = __ldg(rb + w), e = __ldg(rb + w + 1);
-  int4 m = make_int4(0, 0, 0, 0);
-  double wt = 0.0;
-  if (b < e) {
-    m = __ldg(A.items + b);
-    wt = __ldg(A.itw + b);
-  }
-  for (int it = b; it < e; ++it) {
-    // prefetch the next item's descriptor while this one computes
-    int4 mn = m;
-    double wn = wt;
-    if (it + 1 < e) {
-      mn = __ldg(A.items + it + 1);
-      wn = __ldg(A.itw + it + 1);
-    }
-    yc_dispatch<T, J, NOUT>(m.x, sX, lane, m.y, m.z, wt, ar, ai);
-    m = mn;
-    wt = wn;
-  }
-#pragma unroll
-  for (int m = 0; m <= J; ++m) {
-    sred[((w * (J + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
-    sred[((w * (J + 1) + m) * 2 + 1) * 32 + lane] = ai[m];
-  }
-  __syncthreads();
-  const int hb = c_half_off(J) + mb * (J + 1);
-  const int fb = c_full_off(J) + mb * (J + 1);
-  const bool mid = 2 * mb == J;
-  for (int ma = w; ma <= J; ma += nw) {
-    double yr = 0.0, yi = 0.0;
-    for (int q = 0; q < nw; ++q) {
-      yr += sred[((q * (J + 1) + ma) * 2 + 0) * 32 + lane];
-      yi += sred[((q * (J + 1) + ma) * 2 + 1) * 32 + lane];
-    }
-    const double wgt = mid ? ((2 * ma < J) ? 1.0 : ((2 * ma == J) ? 0.5 : 0.0)) : 1.0;
-    yr *= wgt;
-    yi *= wgt;
-    e_acc += yr * sX[(fb + ma) * 32 + lane] + yi * sX[(NF + fb + ma) * 32 + lane];
-    Yt[(size_t)(hb + ma) * 32] = yr;
-    Yt[(size_t)(NH + hb + ma) * 32] = yi;
-  }
-  __syncthreads();
-}
-
-template <int T>
-__global__ void __launch_bounds__(384, 1) k_compute_Y_unrolled(const YCArgs A) {
-  constexpr int NF = c_full_off(T + 1);
-  constexpr int NH = c_half_off(T + 1);
-  extern __shared__ double smem[];
-  double* sX = smem;                  // [re|im][full idx][32]
-  double* sred = smem + 2 * NF * 32;  // [warp][T+1][re|im][32]
-  __shared__ double se[12][32];
-  const int tile = blockIdx.x;
-  const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
-  for (int e = threadIdx.x; e < NF * 32; e += blockDim.x) {
-    const int f = e >> 5, ln = e & 31;
-    const int code = __ldg(A.expand + f);
-    const int src = code >> 2;
-    double re = Vt[src * 32 + ln], im = Vt[(NH + src) * 32 + ln];
-    if (code & 2) im = -im;
-    if (code & 1) {
-      re = -re;
-      im = -im;
-    }
-    sX[f * 32 + ln] = re;
-    sX[(NF + f) * 32 + ln] = im;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
-  double* Yt = A.Y + (size_t)tile * 2 * NH * 32 + lane;
-  double e_acc = 0.0;
-  for (int q = 0;; ++q) {
-    const int code = __ldg(tasks + q);
-    if (code < 0) break;
-    const int j = code >> 6, mb = code & 63;
-    const int rid = c_acc_off(j) + mb;
-#define YCROW(JJ)                                                                       \
-  case JJ:                                                                              \
-    if constexpr (JJ <= T) {                                                            \
-      if (2 * mb == JJ) yc_row<T, JJ, true>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc); \
-      else yc_row<T, JJ, false>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc);          \
-    }                                                                                   \
-    break;
-    switch (j) {
-      YCROW(0) YCROW(1) YCROW(2) YCROW(3) YCROW(4) YCROW(5) YCROW(6) YCROW(7) YCROW(8)
-      default: break;
-    }
-#undef YCROW
-  }
-  se[w][lane] = e_acc;
-  __syncthreads();
-  if (w == 0) {
-    double s = 0.0;
-    for (int q = 0; q < nw; ++q) s += se[q][lane];
-    const int atom = tile * 32 + lane;
-    energy_epilogue(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
-  }
-}
 
 struct YWArgs {
   const double* V;
@@ -919,30 +687,65 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
     const int coff = CWB + (m.z >> 8);
     const double* p1 = sX + (kXPad + m.x) * 32 + lane;  // x1[m.x + k] at p1[k*32]
     const double* p2 = sX + (kXPad + m.y) * 32 + lane;
-    double wr[L], wi[L];
+    // Register window E: E[U-1+ma] = x1[ma + D - a2] (current window); the
+    // U-1 slots below hold the elements entering during a block of U steps,
+    // so step u of a block reads E[U-1+ma-u] (compile-time index) and only
+    // one re-alignment per block is needed.
+    constexpr int U = 3;
+    double er[L + U - 1], ei[L + U - 1];
 #pragma unroll
     for (int ma = 0; ma < L; ++ma) {
-      wr[ma] = p1[ma * 32];
-      wi[ma] = p1[(NP + ma) * 32];
+      er[U - 1 + ma] = p1[ma * 32];
+      ei[U - 1 + ma] = p1[(NP + ma) * 32];
     }
-    for (int a2 = 0; a2 <= J2; ++a2) {
+    int a2 = 0;
+    for (; a2 + U - 1 <= J2; a2 += U) {
+#pragma unroll
+      for (int k = 1; k < U; ++k) {  // x1[D - a2 - k]
+        er[U - 1 - k] = p1[(-a2 - k) * 32];
+        ei[U - 1 - k] = p1[(NP - a2 - k) * 32];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double x2r = wt * p2[(a2 + u) * 32], x2i = wt * p2[(NP + a2 + u) * 32];
+        const double* c = cCW + coff + (a2 + u) * JW;
+#pragma unroll
+        for (int ma = 0; ma < L; ++ma) {
+          const double cc = c[ma];
+          const double wr = er[U - 1 + ma - u], wi = ei[U - 1 + ma - u];
+          const double pr = wr * x2r - wi * x2i;
+          const double pi = wr * x2i + wi * x2r;
+          ar[ma] = fma(cc, pr, ar[ma]);
+          ai[ma] = fma(cc, pi, ai[ma]);
+        }
+      }
+      // re-align: new window = x1[ma + D - a2 - U] = E[ma - 1], E[-1] loaded
+#pragma unroll
+      for (int ma = L - 1; ma >= 1; --ma) {
+        er[U - 1 + ma] = er[ma - 1];
+        ei[U - 1 + ma] = ei[ma - 1];
+      }
+      er[U - 1] = p1[(-a2 - U) * 32];
+      ei[U - 1] = p1[(NP - a2 - U) * 32];
+    }
+    for (; a2 <= J2; ++a2) {  // remainder, one step at a time
       const double x2r = wt * p2[a2 * 32], x2i = wt * p2[(NP + a2) * 32];
       const double* c = cCW + coff + a2 * JW;
 #pragma unroll
       for (int ma = 0; ma < L; ++ma) {
         const double cc = c[ma];
-        const double pr = wr[ma] * x2r - wi[ma] * x2i;
-        const double pi = wr[ma] * x2i + wi[ma] * x2r;
+        const double pr = er[U - 1 + ma] * x2r - ei[U - 1 + ma] * x2i;
+        const double pi = er[U - 1 + ma] * x2i + ei[U - 1 + ma] * x2r;
         ar[ma] = fma(cc, pr, ar[ma]);
         ai[ma] = fma(cc, pi, ai[ma]);
       }
 #pragma unroll
       for (int ma = L - 1; ma > 0; --ma) {
-        wr[ma] = wr[ma - 1];
-        wi[ma] = wi[ma - 1];
+        er[U - 1 + ma] = er[U - 2 + ma];
+        ei[U - 1 + ma] = ei[U - 2 + ma];
       }
-      wr[0] = p1[(-a2 - 1) * 32];
-      wi[0] = p1[(NP - a2 - 1) * 32];
+      er[U - 1] = p1[(-a2 - 1) * 32];
+      ei[U - 1] = p1[(NP - a2 - 1) * 32];
     }
   }
 #pragma unroll

@@ -83,11 +83,11 @@ struct snapgpu_ctx {
 
   // device tables
   DevBuf<double> d_weights, d_itw, d_cw, d_citw;
-  DevBuf<int4> d_items, d_citems;
+  DevBuf<int4> d_items;
   DevBuf<int> d_rowbeg, d_tasks, d_expand, d_rwbeg;
   YPlan yplan;
   YCoopPlan ycplan;
-  int y_impl = 0;  // 2J<=8: 0 constant-window, 1 unrolled, 2 half-V window
+  int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
   DevBuf<int4> d_witems;
   int task_cap = 0;
   int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
@@ -266,28 +266,6 @@ struct LaunchY {
         return;
       }
     }
-    if constexpr (y_unrolled(T)) {
-      constexpr int NF = c_full_off(T + 1);
-      YCArgs a;
-      a.V = c->d_V.p;
-      a.Y = c->d_Y.p;
-      a.expand = c->d_expand.p;
-      a.items = c->d_citems.p;
-      a.itw = c->d_citw.p;
-      a.rw_begin = c->d_rwbeg.p;
-      a.nwarps = c->ycplan.warps;
-      a.tasks = c->d_tasks.p;
-      a.task_cap = c->task_cap;
-      a.nlocal = c->nlocal;
-      a.E = energy_out(c);
-      const size_t smem = sizeof(double) * (2 * NF * 32 + (size_t)c->y_warps * (T + 1) * 2 * 32);
-      CK(cudaFuncSetAttribute(k_compute_Y_unrolled<T>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      dim3 grid(c->ntiles, c->y_parts_used);
-      k_compute_Y_unrolled<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
-      CK(cudaGetLastError());
-      return;
-    }
     constexpr int RED = 8 * (T + 1) * 2 * 32 * 8;
     if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
       if (c->y_ta == 32) return launch<32>(c);
@@ -327,7 +305,7 @@ void build_ycoop(snapgpu_ctx* c);
 void plan_y(snapgpu_ctx* c) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  if (c->y_impl <= 1) {  // one 32-atom tile per CTA, all warps per row
+  if (c->y_impl == 0) {  // one 32-atom tile per CTA, all warps per row
     if (c->ycplan.warps != c->y_warps) build_ycoop(c);
     int parts = c->y_parts;
     // one CTA per SM: never exceed a single wave
@@ -353,7 +331,7 @@ void plan_y(snapgpu_ctx* c) {
 }
 
 void upload_beta(snapgpu_ctx* c) {
-  if (c->y_impl <= 1) {
+  if (c->y_impl == 0) {
     const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
     const std::vector<double> itw = ycoop_weights(c->ycplan, c->maps, W);
     c->d_citw.alloc(std::max<size_t>(1, itw.size()));
@@ -368,12 +346,7 @@ void upload_beta(snapgpu_ctx* c) {
 }
 
 void build_ycoop(snapgpu_ctx* c) {
-  c->ycplan = ycoop_plan(c->maps, c->y_warps);
-  std::vector<int4> it(c->ycplan.items.size());
-  for (size_t q = 0; q < it.size(); ++q)
-    it[q] = make_int4(c->ycplan.items[q][3], c->ycplan.items[q][1], c->ycplan.items[q][2], 0);
-  c->d_citems.alloc(std::max<size_t>(1, it.size()));
-  CK(cudaMemcpy(c->d_citems.p, it.data(), it.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  c->ycplan = ycoop_plan(c->maps, c->y_warps, true);
   if (c->y_impl == 0) {  // constant-window items
     std::vector<int> cwoff(c->maps.tuples.size());
     int o = 0;
@@ -410,17 +383,6 @@ void upload_cwin(int device, int T, const YPlan& p) {
   done.push_back({device, T});
 }
 
-void upload_cprime(int device, int T, const IndexMaps& m, const std::vector<double>& cg) {
-  static std::mutex mu;
-  static std::vector<std::pair<int, int>> done;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& d : done)
-    if (d.first == device && d.second == T) return;
-  const std::vector<double> cp = cprime_table(m, cg);
-  CK(cudaMemcpyToSymbol(cCP, cp.data(), cp.size() * sizeof(double),
-                        static_cast<size_t>(cp_base(T)) * sizeof(double)));
-  done.push_back({device, T});
-}
 
 void launch_U(snapgpu_ctx* c) {
   if (c->nlocal > 0) dispatch_T<LaunchU>(c->T, c);
@@ -635,19 +597,13 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     up(c->d_cw, c->yplan.cw);
     // compute_Y implementation: constant-window (default for 2J <= 8, where
     // the windowed C' fits constant memory), unrolled (2J = 8), half-V window.
-    c->y_impl = 2;
-    if (cw_base(twojmax) >= 0) c->y_impl = 0;
-    if (const char* e = std::getenv("SNAPGPU_Y_IMPL")) {
-      const std::string v(e);
-      if (v == "unrolled" && y_unrolled(twojmax)) c->y_impl = 1;
-      if (v == "window") c->y_impl = 2;
-      if (v == "cwin" && cw_base(twojmax) >= 0) c->y_impl = 0;
-    }
-    if (c->y_impl <= 1) {
+    c->y_impl = (cw_base(twojmax) >= 0) ? 0 : 2;
+    if (const char* e = std::getenv("SNAPGPU_Y_IMPL"))  // A/B switch for development
+      if (std::string(e) == "window") c->y_impl = 2;
+    if (c->y_impl == 0) {
       c->y_warps = 12;
       up(c->d_expand, full_expand_map(c->maps));
-      if (c->y_impl == 1) upload_cprime(device, twojmax, c->maps, c->cg);
-      else upload_cwin(device, twojmax, c->yplan);
+      upload_cwin(device, twojmax, c->yplan);
       build_ycoop(c);  // uploads the beta-dependent item weights
     } else {
       upload_beta(c);
@@ -677,7 +633,7 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_cw.release();
   c->d_items.release();
   c->d_rowbeg.release();
-  c->d_citems.release();
+
   c->d_citw.release();
   c->d_expand.release();
   c->d_rwbeg.release();
@@ -997,7 +953,7 @@ int snapgpu_stage_times(snapgpu_ctx* c, float* out4) {
 int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int y_tile_atoms) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    require(y_warps >= 0 && y_warps <= (c->y_impl <= 1 ? 12 : 8),
+    require(y_warps >= 0 && y_warps <= (c->y_impl == 0 ? 12 : 8),
             "tune: y_warps in [0,12] (2J <= 8) or [0,8]");
     require(y_tile_atoms == 0 || y_tile_atoms == 8 || y_tile_atoms == 16 || y_tile_atoms == 32,
             "tune: y_tile_atoms in {0, 8, 16, 32}");

@@ -276,7 +276,7 @@ std::vector<double> y_item_weights(const IndexMaps& m, const std::vector<double>
   return out;
 }
 
-YCoopPlan ycoop_plan(const IndexMaps& m, int warps) {
+YCoopPlan ycoop_plan(const IndexMaps& m, int warps, bool lpt_split) {
   YCoopPlan p;
   p.warps = warps;
   for (int j = 0; j <= m.T; ++j)
@@ -295,8 +295,9 @@ YCoopPlan ycoop_plan(const IndexMaps& m, int warps) {
           macs += std::max(0, std::min(tp.j1, ma + D) - std::max(0, ma + D - tp.j2) + 1);
         const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
         for (int mb1 = lo; mb1 <= hi; ++mb1) {
-          costs.push_back({6.0 * macs + 2.0 * (tp.j1 + 1) + 4.0 * (tp.j1 + tp.j2 + 2) + 20.0,
-                           static_cast<int>(its.size())});
+          const double c_unrolled = 6.0 * macs + 2.0 * (tp.j1 + 1) + 4.0 * (tp.j1 + tp.j2 + 2) + 20.0;
+          const double c_window = (tp.j2 + 1) * (7.0 * nout + 10.0) + 4.0 * nout + 30.0;
+          costs.push_back({lpt_split ? c_window : c_unrolled, static_cast<int>(its.size())});
           its.push_back({static_cast<int>(q), mb1, mb + D - mb1, local});
         }
       }
@@ -307,7 +308,12 @@ YCoopPlan ycoop_plan(const IndexMaps& m, int warps) {
       // every warp on the same tuple body at the same time (instruction
       // cache locality), with per-warp counts within one of each other.
       std::vector<std::vector<int>> buckets(warps);
-      for (std::size_t i = 0; i < its.size(); ++i) buckets[i % warps].push_back(static_cast<int>(i));
+      if (lpt_split) {  // balance by cost (code-size-insensitive kernels)
+        buckets = lpt(costs, warps);
+        for (auto& bk : buckets) std::sort(bk.begin(), bk.end());
+      } else {
+        for (std::size_t i = 0; i < its.size(); ++i) buckets[i % warps].push_back(static_cast<int>(i));
+      }
       const int base = static_cast<int>(p.items.size());
       int off = base;
       for (int w = 0; w < warps; ++w) {

@@ -96,7 +96,7 @@ struct YCoopPlan {
   std::vector<int> rw_begin;
   std::vector<double> row_cost;
 };
-YCoopPlan ycoop_plan(const IndexMaps& m, int warps);
+YCoopPlan ycoop_plan(const IndexMaps& m, int warps, bool lpt_split);
 std::vector<double> ycoop_weights(const YCoopPlan& p, const IndexMaps& m,
                                   const std::vector<double>& wtab);
 // LPT assignment of rows to workers: [worker][cap] row codes j*64+mb, -1 end.
