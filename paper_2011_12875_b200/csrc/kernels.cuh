@@ -1046,6 +1046,248 @@ __global__ void __launch_bounds__(DECfg<T>::WARPS * 32, (T <= 8 ? 2 : 3))
 }
 
 // ===========================================================================
+// compute_fused_dE, reverse mode.
+//
+// Same (pair, row) lane layout as k_fused_dE, but the Cartesian gradient is
+// obtained by reverse-mode differentiation of the contraction
+//     F = Re sum_{t,e} conj(Y'_t(e)) v_t(e)                (v-space, stored Y')
+// instead of three forward derivative stacks (the reference's
+// wigner_du_level_half, angular_basis.hpp:262-296).  Forward sweep: v level by
+// level in registers, each row's level inputs (its own previous row, or the
+// mirrored seed of a new middle row) saved in lane-private shared memory, F
+// accumulated.  Backward sweep (level 2J..1): adjoints
+//     lambda_t(r,c) = Y'_t(r,c) + a lambda_{t+1}(r,c) - b lambda_{t+1}(r,c+1)
+// (+ the conjugated mirror adjoint of a middle row created at t+1, handed
+// down one lane), with the two complex parameter gradients
+//     G_a += conj(lambda_t(c)) P_t(c),  G_b -= conj(lambda_t(c)) P_t(c-1).
+// Then dF/dx_d = Re(conj(G_a) da_d) + Re(conj(G_b) db_d) and
+//     dE_d = 2 (dsf_d F + sfac dF/dx_d)        (snap_core.hpp:1331-1374).
+// ~30 FP64 instructions per element instead of ~64, and one complex row of
+// registers instead of four.
+// ===========================================================================
+template <int T>
+struct DERCfg {
+  static constexpr int NL = DECfg<T>::NL, G = DECfg<T>::G, PPW = DECfg<T>::PPW;
+  static constexpr int NC = T + 1;
+  static constexpr int NH = c_half_off(T + 1);
+  static constexpr int NIN = T * (T + 1) / 2 > 0 ? T * (T + 1) / 2 : 1;  // inputs of row 0
+  static constexpr int WARPS = (NIN * 2 * 32 * 8 * 4 <= 80 * 1024) ? 4 : 2;
+  static constexpr int SMEM = WARPS * NIN * 2 * 32 * 8;
+};
+
+template <int T>
+__global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
+    k_fused_dE_rev(const DEArgs A) {
+  using C = DERCfg<T>;
+  extern __shared__ double sbuf[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = lane % C::G, q = lane / C::G;
+  const int p = (blockIdx.x * C::WARPS + w) * C::PPW + q;
+  const int S = A.pr.stride;
+  const int i = p / S, k = p - i * S;
+  const bool valid = (p < A.nslots) && (k < A.pr.numneigh[min(i, A.pr.nlocal - 1)]);
+  double x = 1.0, y = 0.0, z = 0.0, wt = 0.0;
+  if (valid) {
+    const double* d = A.pr.disp + (size_t)p * 3;
+    x = d[0];
+    y = d[1];
+    z = d[2];
+    wt = neighbor_weight(A.pr, A.pr.nbr[p]);
+  }
+  PairGeo g;
+  pair_geometry<true>(x, y, z, wt, A.gp, g);
+  const int ia = valid ? i : 0;
+  const double* Yr = A.Y + (size_t)(ia >> 5) * 2 * C::NH * 32 + (ia & 31);
+  const double* Yi = Yr + (size_t)C::NH * 32;
+  double* buf = sbuf + (size_t)w * C::NIN * 2 * 32 + lane;  // [elem][re|im][lane]
+  const int s0 = (2 * r > 1) ? 2 * r : 1;                    // first level whose input row r stores
+  auto in_off = [&](int t) { return (t * (t - 1) - s0 * (s0 - 1)) / 2; };
+  const double ar = g.ar, ai = g.ai, br = g.br, bi = g.bi;
+
+  // ---------------- forward ----------------
+  double vr[C::NC], vi[C::NC];
+#pragma unroll
+  for (int c = 0; c < C::NC; ++c) vr[c] = vi[c] = 0.0;
+  vr[0] = (r == 0) ? 1.0 : 0.0;
+  double F = (r == 0) ? Yr[0] : 0.0;
+#pragma unroll
+  for (int t = 1; t <= T; ++t) {
+    if ((t & 1) == 0 && t < T + (T & 1)) {  // seed the new middle row t/2
+      const bool creator = (2 * r == t);
+      const double R = mirror_R(t);
+#pragma unroll
+      for (int c = 0; c < t; ++c) {
+        const double K = (((c + t / 2) & 1) ? -R : R);
+        const double sr = __shfl_up_sync(0xffffffffu, vr[t - 1 - c], 1);
+        const double si = __shfl_up_sync(0xffffffffu, vi[t - 1 - c], 1);
+        if (creator) {
+          vr[c] = K * sr;
+          vi[c] = -K * si;
+        }
+      }
+    }
+    const bool active = 2 * r <= t;
+    if (active) {
+      const int o = in_off(t);
+#pragma unroll
+      for (int c = 0; c < t; ++c) {
+        buf[(size_t)(2 * (o + c)) * 32] = vr[c];
+        buf[(size_t)(2 * (o + c) + 1) * 32] = vi[c];
+      }
+    }
+    if (t == T && (T & 1) == 0 && 2 * r + 2 == T) {  // transient last middle row
+      const double R = mirror_R(T);
+      const int hb = c_half_off(T) + (T / 2) * (T + 1);
+      double plr = 0.0, pli = 0.0;
+#pragma unroll
+      for (int c = 0; c <= T / 2; ++c) {
+        const double K = (((c + T / 2) & 1) ? -R : R);
+        const double pr = K * vr[T - 1 - c], pi = -K * vi[T - 1 - c];
+        const double nr = ar * pr + ai * pi - br * plr - bi * pli;
+        const double ni = ar * pi - ai * pr - br * pli + bi * plr;
+        F += nr * Yr[(size_t)(hb + c) * 32] + ni * Yi[(size_t)(hb + c) * 32];
+        plr = pr;
+        pli = pi;
+      }
+    }
+    if (active) {
+      const int hb = c_half_off(t) + r * (t + 1);
+#pragma unroll
+      for (int c = t; c >= 0; --c) {
+        const double pr = (c < t) ? vr[c] : 0.0, pi = (c < t) ? vi[c] : 0.0;
+        const double qr = (c > 0) ? vr[c - 1] : 0.0, qi = (c > 0) ? vi[c - 1] : 0.0;
+        const double nr = ar * pr + ai * pi - br * qr - bi * qi;
+        const double ni = ar * pi - ai * pr - br * qi + bi * qr;
+        vr[c] = nr;
+        vi[c] = ni;
+        F += nr * Yr[(size_t)(hb + c) * 32] + ni * Yi[(size_t)(hb + c) * 32];
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---------------- backward ----------------
+  double Gar = 0.0, Gai = 0.0, Gbr = 0.0, Gbi = 0.0;
+  double lr[C::NC], li[C::NC];  // lambda_t(r, c)
+#pragma unroll
+  for (int c = 0; c < C::NC; ++c) lr[c] = li[c] = 0.0;
+  if (2 * r <= T) {
+    const int hb = c_half_off(T) + r * (T + 1);
+#pragma unroll
+    for (int c = 0; c <= T; ++c) {
+      lr[c] = Yr[(size_t)(hb + c) * 32];
+      li[c] = Yi[(size_t)(hb + c) * 32];
+    }
+  }
+#pragma unroll
+  for (int t = T; t >= 1; --t) {
+    const bool active = 2 * r <= t;
+    // adjoints of the level-t inputs; become lambda_{t-1} (+ Y'_{t-1})
+    double gr_[C::NC], gi_[C::NC];
+#pragma unroll
+    for (int c = 0; c < C::NC; ++c) gr_[c] = gi_[c] = 0.0;
+    const int o = in_off(t);
+    if (active) {
+#pragma unroll
+      for (int c = 0; c < t; ++c) {
+        const double pr = buf[(size_t)(2 * (o + c)) * 32];
+        const double pi = buf[(size_t)(2 * (o + c) + 1) * 32];
+        // input P(c) feeds element c (coefficient conj a) and c+1 (-conj b)
+        Gar += lr[c] * pr + li[c] * pi;
+        Gai += lr[c] * pi - li[c] * pr;
+        Gbr -= lr[c + 1] * pr + li[c + 1] * pi;
+        Gbi -= lr[c + 1] * pi - li[c + 1] * pr;
+        gr_[c] = ar * lr[c] - ai * li[c] - br * lr[c + 1] + bi * li[c + 1];
+        gi_[c] = ar * li[c] + ai * lr[c] - br * li[c + 1] - bi * lr[c + 1];
+      }
+    }
+    if (t == T && (T & 1) == 0 && 2 * r + 2 == T) {
+      // transient last middle row: lambda_T(T/2, c) = Y'_T(T/2, c), c <= T/2;
+      // its seed pm(c) = K_c conj(v_{T-1}(r, T-1-c)) is this lane's own
+      // level-T input, so the mirror adjoint lands in gr_[T-1-c].
+      const double R = mirror_R(T);
+      const int hb = c_half_off(T) + (T / 2) * (T + 1);
+      double nlr = 0.0, nli = 0.0;  // lambda(c+1)
+#pragma unroll
+      for (int c = T / 2; c >= 0; --c) {
+        const double K = (((c + T / 2) & 1) ? -R : R);
+        const double tlr = Yr[(size_t)(hb + c) * 32], tli = Yi[(size_t)(hb + c) * 32];
+        const double ur = buf[(size_t)(2 * (o + T - 1 - c)) * 32];
+        const double ui = buf[(size_t)(2 * (o + T - 1 - c) + 1) * 32];
+        const double pr = K * ur, pi = -K * ui;  // pm(c)
+        Gar += tlr * pr + tli * pi;
+        Gai += tlr * pi - tli * pr;
+        Gbr -= nlr * pr + nli * pi;
+        Gbi -= nlr * pi - nli * pr;
+        const double gr = ar * tlr - ai * tli - br * nlr + bi * nli;
+        const double gi = ar * tli + ai * tlr - br * nli - bi * nlr;
+        gr_[T - 1 - c] += K * gr;  // conj, times K
+        gi_[T - 1 - c] -= K * gi;
+        nlr = tlr;
+        nli = tli;
+      }
+    }
+    // a row created at level t (2r == t) hands the conjugated mirror adjoint
+    // of its seed to row r-1 (one lane down), column t-1-c
+    if ((t & 1) == 0 && t < T + (T & 1)) {
+      const double R = mirror_R(t);
+      const bool recv = (2 * r + 2 == t);
+      double sr_[C::NC], si_[C::NC];
+#pragma unroll
+      for (int c = 0; c < t; ++c) {
+        const double K = (((c + t / 2) & 1) ? -R : R);
+        sr_[c] = __shfl_down_sync(0xffffffffu, K * gr_[c], 1);
+        si_[c] = __shfl_down_sync(0xffffffffu, -K * gi_[c], 1);
+      }
+#pragma unroll
+      for (int c = 0; c < t; ++c) {
+        gr_[t - 1 - c] += recv ? sr_[c] : 0.0;
+        gi_[t - 1 - c] += recv ? si_[c] : 0.0;
+      }
+    }
+    // lambda_{t-1} for rows that already existed at level t-1
+    if (t > 1) {
+      const bool keep = 2 * r <= t - 1;
+      const int hb = c_half_off(t - 1) + r * t;
+#pragma unroll
+      for (int c = 0; c < t; ++c) {
+        lr[c] = keep ? Yr[(size_t)(hb + c) * 32] + gr_[c] : 0.0;
+        li[c] = keep ? Yi[(size_t)(hb + c) * 32] + gi_[c] : 0.0;
+      }
+      lr[t] = li[t] = 0.0;
+    }
+  }
+  // reduce the row-lanes of the pair
+#pragma unroll
+  for (int o = 1; o < C::G; o <<= 1) {
+    F += __shfl_xor_sync(0xffffffffu, F, o);
+    Gar += __shfl_xor_sync(0xffffffffu, Gar, o);
+    Gai += __shfl_xor_sync(0xffffffffu, Gai, o);
+    Gbr += __shfl_xor_sync(0xffffffffu, Gbr, o);
+    Gbi += __shfl_xor_sync(0xffffffffu, Gbi, o);
+  }
+  if (valid && r == 0) {
+    double* o = A.dedr + (size_t)p * 3;
+    double de[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double dF = Gar * g.dar[d] + Gai * g.dai[d] + Gbr * g.dbr[d] + Gbi * g.dbi[d];
+      de[d] = 2.0 * (g.dsf[d] * F + g.sfac * dF);
+      o[d] = de[d];
+    }
+    if (A.forces) {
+      double* fi = A.forces + (size_t)(A.pr.atom_lo + i) * 3;
+      double* fj = A.forces + (size_t)A.pr.nbr[p] * 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        atomicAdd(fi + d, de[d]);
+        atomicAdd(fj + d, -de[d]);
+      }
+    }
+  }
+}
+
+// ===========================================================================
 // scatter_forces (snap_core.hpp:872-953, concurrent-RMW strategy):
 // F_i += dE(i,k), F_{nbr} -= dE(i,k) with FP64 RED atomics.
 // ===========================================================================

@@ -88,6 +88,7 @@ struct snapgpu_ctx {
   YPlan yplan;
   YCoopPlan ycplan;
   int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
+  int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
   DevBuf<int4> d_witems;
   int task_cap = 0;
   int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
@@ -288,6 +289,18 @@ struct LaunchDE {
     a.dedr = c->d_dedr.p;
     a.forces = c->fuse_scatter ? c->d_forces.p : nullptr;
     a.nslots = c->nlocal * c->stride;
+    if (c->de_impl == 0) {  // reverse mode
+      using R = DERCfg<T>;
+      const int per_block = R::WARPS * R::PPW;
+      const int blocks = (a.nslots + per_block - 1) / per_block;
+      if (blocks > 0) {
+        CK(cudaFuncSetAttribute(k_fused_dE_rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                R::SMEM));
+        k_fused_dE_rev<T><<<blocks, R::WARPS * 32, R::SMEM, c->stream>>>(a);
+        CK(cudaGetLastError());
+      }
+      return;
+    }
     const int per_block = C::WARPS * C::PPW;
     const int blocks = (a.nslots + per_block - 1) / per_block;
     if (blocks > 0) {
@@ -598,6 +611,9 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     // compute_Y implementation: constant-window (default for 2J <= 8, where
     // the windowed C' fits constant memory), unrolled (2J = 8), half-V window.
     c->y_impl = (cw_base(twojmax) >= 0) ? 0 : 2;
+    c->de_impl = (twojmax <= 10) ? 0 : 1;  // reverse mode needs ~8 register rows
+    if (const char* e = std::getenv("SNAPGPU_DE_IMPL"))  // A/B switch for development
+      c->de_impl = (std::string(e) == "forward") ? 1 : 0;
     if (const char* e = std::getenv("SNAPGPU_Y_IMPL"))  // A/B switch for development
       if (std::string(e) == "window") c->y_impl = 2;
     if (c->y_impl == 0) {
