@@ -20,7 +20,9 @@
 //
 // HBM layouts:
 //   V  (ulisttot, v-space)       [atom/32][re|im][half idx][atom%32]  (AoSoA 32,
-//   Y' (ylist, v-space, weighted) same                                 split planes)
+//                                                                      split planes)
+//   Y' (ylist, v-space, weighted) [atom][half idx][re,im]  (atom-major: the
+//                                  fused dE kernel reads one atom per pair)
 //   dedr                          [atom][slot][3]
 //   forces                        [atom][3]
 #pragma once
@@ -565,8 +567,7 @@ __device__ __forceinline__ void y_row(const double* __restrict__ sV, double* __r
         e_acc += yr * sV[(hb + ma) * TA + ln] + yi * sV[(NH + hb + ma) * TA + ln];
     }
     if (sub == 0) {
-      Yt[(size_t)(hb + ma) * 32] = yr;
-      Yt[(size_t)(NH + hb + ma) * 32] = yi;
+      reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
     }
   }
   __syncthreads();
@@ -589,7 +590,7 @@ __global__ void __launch_bounds__(256) k_compute_Y(const YArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
   const int atom = atom0 + (lane % TA);
-  double* Yt = A.Y + (size_t)(atom >> 5) * 2 * NH * 32 + (atom & 31);
+  double* Yt = A.Y + (size_t)atom * NH * 2;  // Y' atom-major, interleaved complex
   double e_acc = 0.0;
   for (int q = 0;; ++q) {
     const int code = __ldg(tasks + q);
@@ -768,8 +769,7 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
       yi *= wgt;
       e_acc += yr * sX[(fb + ma) * 32 + lane] + yi * sX[(NP + fb + ma) * 32 + lane];
     }
-    Yt[(size_t)(hb + ma) * 32] = yr;
-    Yt[(size_t)(NH + hb + ma) * 32] = yi;
+    reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
   }
   __syncthreads();
 }
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(384, 1) k_compute_Y_cwin(const YWArgs A) {
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
-  double* Yt = A.Y + (size_t)tile * 2 * NH * 32 + lane;
+  double* Yt = A.Y + (size_t)(tile * 32 + lane) * NH * 2;  // Y' atom-major, interleaved complex
   double e_acc = 0.0;
   for (int q = 0;; ++q) {
     const int code = __ldg(tasks + q);
@@ -888,10 +888,9 @@ __global__ void __launch_bounds__(DECfg<T>::WARPS * 32, (T <= 8 ? 2 : 3))
   PairGeo g;
   pair_geometry<true>(x, y, z, wt, A.gp, g);
   const int ia = valid ? i : 0;
-  const double* Yr = A.Y + (size_t)(ia >> 5) * 2 * C::NH * 32 + (ia & 31);
-  const double* Yi = Yr + (size_t)C::NH * 32;
+  const double2* Y2 = reinterpret_cast<const double2*>(A.Y) + (size_t)ia * C::NH;
 
-  double Au = (r == 0) ? Yr[0] : 0.0;  // level 0: v = 1
+  double Au = (r == 0) ? __ldg(Y2).x : 0.0;  // level 0: v = 1
   double Ad[3] = {0.0, 0.0, 0.0};
   const double ar = g.ar, ai = g.ai, br = g.br, bi = g.bi;
 
@@ -969,7 +968,8 @@ __global__ void __launch_bounds__(DECfg<T>::WARPS * 32, (T <= 8 ? 2 : 3))
             }
             const double nr = ar * pr + ai * pi - br * plr - bi * pli;
             const double ni = ar * pi - ai * pr - br * pli + bi * plr;
-            const double yr = Yr[(size_t)(hb + c) * 32], yi = Yi[(size_t)(hb + c) * 32];
+            const double2 yv = __ldg(Y2 + hb + c);
+            const double yr = yv.x, yi = yv.y;
             if (pass == 0) au += nr * yr + ni * yi;
 #pragma unroll
             for (int d = 0; d < NDIR; ++d) {
@@ -993,7 +993,8 @@ __global__ void __launch_bounds__(DECfg<T>::WARPS * 32, (T <= 8 ? 2 : 3))
         for (int c = t; c >= 0; --c) {
           const double pr = (c < t) ? vr[c] : 0.0, pi = (c < t) ? vi[c] : 0.0;
           const double qr = (c > 0) ? vr[c - 1] : 0.0, qi = (c > 0) ? vi[c - 1] : 0.0;
-          const double yr = Yr[(size_t)(hb + c) * 32], yi = Yi[(size_t)(hb + c) * 32];
+          const double2 yv = __ldg(Y2 + hb + c);
+            const double yr = yv.x, yi = yv.y;
 #pragma unroll
           for (int d = 0; d < NDIR; ++d) {
             const double dpr = (c < t) ? dvr[d][c] : 0.0, dpi = (c < t) ? dvi[d][c] : 0.0;
@@ -1097,8 +1098,7 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
   PairGeo g;
   pair_geometry<true>(x, y, z, wt, A.gp, g);
   const int ia = valid ? i : 0;
-  const double* Yr = A.Y + (size_t)(ia >> 5) * 2 * C::NH * 32 + (ia & 31);
-  const double* Yi = Yr + (size_t)C::NH * 32;
+  const double2* Y2 = reinterpret_cast<const double2*>(A.Y) + (size_t)ia * C::NH;
   double* buf = sbuf + (size_t)w * C::NIN * 2 * 32 + lane;  // [elem][re|im][lane]
   const int s0 = (2 * r > 1) ? 2 * r : 1;                    // first level whose input row r stores
   auto in_off = [&](int t) { return (t * (t - 1) - s0 * (s0 - 1)) / 2; };
@@ -1109,7 +1109,7 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
 #pragma unroll
   for (int c = 0; c < C::NC; ++c) vr[c] = vi[c] = 0.0;
   vr[0] = (r == 0) ? 1.0 : 0.0;
-  double F = (r == 0) ? Yr[0] : 0.0;
+  double F = (r == 0) ? __ldg(Y2).x : 0.0;
 #pragma unroll
   for (int t = 1; t <= T; ++t) {
     if ((t & 1) == 0 && t < T + (T & 1)) {  // seed the new middle row t/2
@@ -1145,7 +1145,10 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
         const double pr = K * vr[T - 1 - c], pi = -K * vi[T - 1 - c];
         const double nr = ar * pr + ai * pi - br * plr - bi * pli;
         const double ni = ar * pi - ai * pr - br * pli + bi * plr;
-        F += nr * Yr[(size_t)(hb + c) * 32] + ni * Yi[(size_t)(hb + c) * 32];
+        {
+          const double2 yv = __ldg(Y2 + hb + c);
+          F += nr * yv.x + ni * yv.y;
+        }
         plr = pr;
         pli = pi;
       }
@@ -1160,7 +1163,10 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
         const double ni = ar * pi - ai * pr - br * qi + bi * qr;
         vr[c] = nr;
         vi[c] = ni;
-        F += nr * Yr[(size_t)(hb + c) * 32] + ni * Yi[(size_t)(hb + c) * 32];
+        {
+          const double2 yv = __ldg(Y2 + hb + c);
+          F += nr * yv.x + ni * yv.y;
+        }
       }
     }
   }
@@ -1175,8 +1181,9 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
     const int hb = c_half_off(T) + r * (T + 1);
 #pragma unroll
     for (int c = 0; c <= T; ++c) {
-      lr[c] = Yr[(size_t)(hb + c) * 32];
-      li[c] = Yi[(size_t)(hb + c) * 32];
+      const double2 yv = __ldg(Y2 + hb + c);
+      lr[c] = yv.x;
+      li[c] = yv.y;
     }
   }
 #pragma unroll
@@ -1211,7 +1218,8 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
 #pragma unroll
       for (int c = T / 2; c >= 0; --c) {
         const double K = (((c + T / 2) & 1) ? -R : R);
-        const double tlr = Yr[(size_t)(hb + c) * 32], tli = Yi[(size_t)(hb + c) * 32];
+        const double2 yv = __ldg(Y2 + hb + c);
+        const double tlr = yv.x, tli = yv.y;
         const double ur = buf[(size_t)(2 * (o + T - 1 - c)) * 32];
         const double ui = buf[(size_t)(2 * (o + T - 1 - c) + 1) * 32];
         const double pr = K * ur, pi = -K * ui;  // pm(c)
@@ -1251,8 +1259,9 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
       const int hb = c_half_off(t - 1) + r * t;
 #pragma unroll
       for (int c = 0; c < t; ++c) {
-        lr[c] = keep ? Yr[(size_t)(hb + c) * 32] + gr_[c] : 0.0;
-        li[c] = keep ? Yi[(size_t)(hb + c) * 32] + gi_[c] : 0.0;
+        const double2 yv = keep ? __ldg(Y2 + hb + c) : make_double2(0.0, 0.0);
+        lr[c] = keep ? yv.x + gr_[c] : 0.0;
+        li[c] = keep ? yv.y + gi_[c] : 0.0;
       }
       lr[t] = li[t] = 0.0;
     }

@@ -844,7 +844,7 @@ int snapgpu_get_ylist(snapgpu_ctx* c, double* out) {
     const IndexMaps& m = c->maps;
     const int NH = m.nhalf;
     for (int a = 0; a < c->nlocal; ++a) {
-      const size_t base = (size_t)(a >> 5) * 2 * NH * 32 + (a & 31);
+      const size_t base = (size_t)a * NH * 2;  // Y' atom-major, interleaved complex
       double* o = out + (size_t)a * NH * 2;
       for (int t = 0; t <= m.T; ++t)
         for (int mb = 0; 2 * mb <= t; ++mb)
@@ -852,8 +852,8 @@ int snapgpu_get_ylist(snapgpu_ctx* c, double* out) {
             const int e = m.half_off[t] + mb * (t + 1) + ma;
             if (c->ywgt[e] != 0.0) {
               const double s = c->hf[e] / c->ywgt[e];
-              o[2 * e] = h[base + (size_t)e * 32] * s;
-              o[2 * e + 1] = h[base + (size_t)(NH + e) * 32] * s;
+              o[2 * e] = h[base + 2 * e] * s;
+              o[2 * e + 1] = h[base + 2 * e + 1] * s;
             }
           }
       // middle-row elements ma > t/2 are never computed on the device; they
