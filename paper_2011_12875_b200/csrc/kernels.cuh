@@ -1077,7 +1077,7 @@ struct DERCfg {
 };
 
 template <int T>
-__global__ void __launch_bounds__(DERCfg<T>::WARPS * 32)
+__global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
     k_fused_dE_rev(const DEArgs A) {
   using C = DERCfg<T>;
   extern __shared__ double sbuf[];

@@ -11,11 +11,21 @@ KEYS = ['gpu__time_duration.sum', 'smsp__issue_active.avg.pct_of_peak_sustained_
 def run(path):
     raw = subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
+    scale = {'byte': 1.0, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}
     out = []
     for r in rows[2:]:
         d = {'kernel': r[h.index('Kernel Name')][:40]}
-        d.update({k: r[h.index(k)] for k in KEYS if k in h})
+        for k in KEYS:
+            if k not in h:
+                continue
+            i = h.index(k)
+            v = r[i]
+            if units[i] in scale:  # normalise byte counts
+                v = float(v.replace(',', '')) * scale[units[i]]
+            elif units[i]:
+                v = f"{v} {units[i]}"
+            d[k] = v
         st = {}
         for k in h:
             if k.startswith('smsp__pcsamp_warps_issue_stalled_') and not k.endswith('not_issued'):
@@ -28,15 +38,34 @@ def run(path):
     src = subprocess.run(['ncu', '-i', path, '--page', 'source', '--csv', '--print-source', 'sass'],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
-    if len(rows) > 2:
-        hdr = rows[1]
-        iS, iE = hdr.index('Source'), hdr.index('Instructions Executed')
-        c = Counter()
-        for r in rows[2:]:
-            op = re.sub(r'^@!?U?P\w+\s+', '', r[iS].strip()).split(' ')[0].split('.')[0]
-            c[op] += int(r[iE]) if r[iE].isdigit() else 0
-        T = sum(c.values()) or 1
-        out[-1]['mix'] = [(k, round(v / T * 100, 1)) for k, v in c.most_common(12)]
+    # one section per kernel: a "Kernel Name" line, a header, then rows
+    cur, hdr, c = None, None, None
+    mixes = []
+    for r in rows:
+        if r and r[0] == 'Kernel Name':
+            if c is not None:
+                mixes.append((cur, c))
+            cur, c, hdr = r[1], Counter(), None
+            continue
+        if hdr is None:
+            hdr = r
+            iS, iE = hdr.index('Source'), hdr.index('Instructions Executed')
+            continue
+        if len(r) <= max(iS, iE):
+            continue
+        op = re.sub(r'^@!?U?P\w+\s+', '', r[iS].strip()).split(' ')[0].split('.')[0]
+        c[op] += int(r[iE]) if r[iE].isdigit() else 0
+    if c is not None:
+        mixes.append((cur, c))
+    merged = {}
+    for name, m in mixes:  # the page lists each kernel more than once: keep the richest
+        if sum(m.values()) > sum(merged.get(name, Counter()).values()):
+            merged[name] = m
+    order = list(dict.fromkeys(n for n, _ in mixes))
+    for d, name in zip(out, order):
+        m = merged[name]
+        T = sum(m.values()) or 1
+        d['mix'] = [(k, round(v / T * 100, 1)) for k, v in m.most_common(12)]
     return out
 
 if __name__ == '__main__':
