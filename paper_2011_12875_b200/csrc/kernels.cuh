@@ -189,7 +189,8 @@ struct UArgs {
 template <int T>
 struct UCfg {
   static constexpr int NC = T + 1;
-  static constexpr int NSLOT = 32 / NC;
+  static constexpr int SW = T + 2;  // lanes per pair slot: guard + T+1 columns
+  static constexpr int NSLOT = 32 / SW;
   static constexpr int NROW = T / 2 + 1;
   static constexpr int NACC = c_acc_off(T + 1);
   static constexpr int NH = c_half_off(T + 1);
@@ -258,16 +259,19 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32)
   }
   __syncwarp();
 
-  const int slot = lane / C::NC;
-  const int c = lane - slot * C::NC;
-  const int sbase = slot * C::NC;
+  // Slot = T+2 lanes: a guard lane (column -1, value always 0) followed by the
+  // T+1 columns, so edge columns and invalid mirror sources read exact zeros
+  // from the guard instead of needing selects.
+  const int slot = lane / C::SW;
+  const int c = lane - slot * C::SW - 1;  // column, -1 = guard
+  const int sbase = slot * C::SW + 1;     // lane of column 0
   UAcc<T, C::REGACC> acc;
   acc.init(accs, lane);
 
   for (int k0 = 0; k0 < nn; k0 += C::NSLOT) {
     const int k = k0 + slot;
     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0, sf = 0.0;
-    if (slot < C::NSLOT && k < nn) {
+    if (slot < C::NSLOT && k < nn && c >= 0) {
       ar = geo[k * 5 + 0];
       ai = geo[k * 5 + 1];
       br = geo[k * 5 + 2];
@@ -277,36 +281,34 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32)
     double vr[C::NROW], vi[C::NROW];
 #pragma unroll
     for (int mb = 0; mb < C::NROW; ++mb) vr[mb] = vi[mb] = 0.0;
-    vr[0] = (c == 0) ? 1.0 : 0.0;
+    vr[0] = (c == 0 && sf != 0.0) ? 1.0 : 0.0;
     acc.add(0, sf, vr[0], 0.0);
 #pragma unroll
     for (int t = 1; t <= T; ++t) {
-      // left-column values of the rows that exist at level t-1
+      // left-column values of the rows that exist at level t-1 (guard -> 0)
       double qr[C::NROW], qi[C::NROW];
 #pragma unroll
       for (int mb = 0; 2 * mb <= t - 1; ++mb) {
-        const double sr = __shfl_up_sync(0xffffffffu, vr[mb], 1);
-        const double si = __shfl_up_sync(0xffffffffu, vi[mb], 1);
-        qr[mb] = (c == 0) ? 0.0 : sr;
-        qi[mb] = (c == 0) ? 0.0 : si;
+        qr[mb] = __shfl_up_sync(0xffffffffu, vr[mb], 1);
+        qi[mb] = __shfl_up_sync(0xffffffffu, vi[mb], 1);
       }
       double pmr = 0.0, pmi = 0.0, qmr = 0.0, qmi = 0.0;
       if ((t & 1) == 0) {
-        // new middle row t/2 from the mirror of row t/2-1 at level t-1
+        // new middle row t/2 from the mirror of row t/2-1 at level t-1;
+        // invalid sources are the slot's guard lane (zero)
         const int m = t / 2 - 1;
-        const bool ok1 = c <= t - 1, ok2 = (c >= 1) && (c <= t);
-        const int src1 = sbase + (ok1 ? (t - 1 - c) : 0);
-        const int src2 = sbase + (ok2 ? (t - c) : 0);
+        const int src1 = (c >= 0 && c <= t - 1) ? sbase + (t - 1 - c) : sbase - 1;
+        const int src2 = (c >= 1 && c <= t) ? sbase + (t - c) : sbase - 1;
         const double s1r = __shfl_sync(0xffffffffu, vr[m], src1);
         const double s1i = __shfl_sync(0xffffffffu, vi[m], src1);
         const double s2r = __shfl_sync(0xffffffffu, vr[m], src2);
         const double s2i = __shfl_sync(0xffffffffu, vi[m], src2);
         const double R = mirror_R(t);
         const double sg = ((c + t / 2) & 1) ? -R : R;  // (-1)^(c+t/2) R
-        pmr = ok1 ? sg * s1r : 0.0;
-        pmi = ok1 ? -sg * s1i : 0.0;
-        qmr = ok2 ? -sg * s2r : 0.0;  // (-1)^(c-1+t/2) R
-        qmi = ok2 ? sg * s2i : 0.0;
+        pmr = sg * s1r;
+        pmi = -sg * s1i;
+        qmr = -sg * s2r;  // (-1)^(c-1+t/2) R
+        qmi = sg * s2i;
       }
 #pragma unroll
       for (int mb = 0; 2 * mb <= t - 1; ++mb) {
@@ -331,13 +333,13 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32)
     double r = acc.getr(q), im = acc.geti(q);
 #pragma unroll
     for (int s = 1; s < C::NSLOT; ++s) {
-      r += __shfl_down_sync(0xffffffffu, acc.getr(q), s * C::NC);
-      im += __shfl_down_sync(0xffffffffu, acc.geti(q), s * C::NC);
+      r += __shfl_down_sync(0xffffffffu, acc.getr(q), s * C::SW);
+      im += __shfl_down_sync(0xffffffffu, acc.geti(q), s * C::SW);
     }
     outr[q] = r;
     outi[q] = im;
   }
-  if (slot == 0) {
+  if (slot == 0 && c >= 0) {
     const int tile = i >> 5, ln = i & 31;
     double* Vr = A.V + ((size_t)tile * 2 * C::NH) * 32 + ln;
     double* Vi = Vr + (size_t)C::NH * 32;
