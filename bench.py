@@ -318,18 +318,19 @@ def run_ours(args):
         pin = [torch.from_numpy(a).pin_memory() for a in own]
         host_np = [t.numpy() for t in pin]
         f_host = torch.zeros((N, 3), dtype=torch.float64).pin_memory()
-        e_host = np.zeros(natoms_local)
+        e_host = torch.zeros(natoms_local, dtype=torch.float64).pin_memory().numpy()
+        t_host = torch.zeros(1, dtype=torch.float64).pin_memory().numpy()
         h2d = sum(a.nbytes for a in host_np)
         d2h = (pe.f_own.numel() if n_gpus > 1 else N * 3) * 8 + natoms_local * 8 + 8
 
         def e2e_step():
-            pe.upload(*host_np)
-            step()
-            if n_gpus == 1:
-                eng.forces(f_host.numpy())
+            if n_gpus == 1:  # the public one-call API: upload, run, read back
+                eng.step(*host_np, forces=f_host.numpy(), eatom=e_host, etotal=t_host)
             else:
+                pe.upload(*host_np)
+                step()
                 f_host.view(-1)[: pe.f_own.numel()].copy_(pe.f_own, non_blocking=False)
-            eng.energy()
+                eng.energy()
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()

@@ -106,6 +106,16 @@ int snapgpu_scatter_forces(snapgpu_ctx* ctx);    /* scatter_forces   :872  */
 int snapgpu_run(snapgpu_ctx* ctx);
 int snapgpu_synchronize(snapgpu_ctx* ctx);
 
+/* One force step from host buffers (the end-to-end call): upload the owned
+ * atoms' lists (set_neighbors_partition semantics; atom_lo = 0 and nlocal =
+ * natoms_total for a single GPU), run, and copy forces (natoms_total x 3),
+ * eatom (nlocal) and etotal back (any output may be NULL); one stream
+ * synchronization.  Equivalent to run_pipeline (pipeline.hpp:206-303). */
+int snapgpu_run_host(snapgpu_ctx* ctx, int natoms_total, int atom_lo, int nlocal,
+                     int stride, const int* numneigh, const int* nbr,
+                     const double* disp, const int* types, double* forces,
+                     double* eatom, double* etotal);
+
 /* ---- results (host copies; synchronize the stream) ---------------------
  * forces: natoms_total x 3 (PipelineResult::forces, pipeline.hpp:50);
  * eatom: nlocal (EnergyReport::per_atom); etotal: sum over owned atoms. */

@@ -82,6 +82,7 @@ def library() -> C.CDLL:
     for f in ("compute_U", "compute_Y", "compute_dU_deidrj", "scatter_forces", "run",
               "synchronize"):
         getattr(L, "snapgpu_" + f).argtypes = [vp]
+    L.snapgpu_run_host.argtypes = [vp, ip, ip, ip, ip, vp, vp, vp, vp, vp, vp, vp]
     L.snapgpu_get_forces.argtypes = [vp, vp]
     L.snapgpu_get_energy.argtypes = [vp, vp, vp]
     L.snapgpu_get_ulisttot.argtypes = [vp, vp]
@@ -298,6 +299,28 @@ class SnapEngine:
     def run(self):
         self._c(self._L.snapgpu_run(self._h))
 
+    def step(self, numneigh, nbr, disp, types=None, forces=None, eatom=None, etotal=None,
+             natoms_total=None, atom_lo=0):
+        """One end-to-end force step from host arrays (snapgpu_run_host): upload,
+        run, read back; outputs are written into the given (ideally pinned)
+        arrays when provided.  Returns (forces, eatom, etotal)."""
+        nn = np.ascontiguousarray(numneigh, np.int32)
+        nb = np.ascontiguousarray(nbr, np.int32)
+        dp = np.ascontiguousarray(disp, np.float64)
+        ty = None if types is None else np.ascontiguousarray(types, np.int32)
+        n = int(nn.shape[0])
+        stride = int(nb.shape[1]) if nb.ndim == 2 else int(nb.size // max(n, 1))
+        ntot = n if natoms_total is None else int(natoms_total)
+        f = forces if forces is not None else np.zeros((ntot, 3), np.float64)
+        e = eatom if eatom is not None else np.zeros(n, np.float64)
+        t = etotal if etotal is not None else np.zeros(1, np.float64)
+        self._c(self._L.snapgpu_run_host(self._h, ntot, int(atom_lo), n, stride, nn.ctypes.data,
+                                         nb.ctypes.data, dp.ctypes.data, _ptr(ty),
+                                         f.ctypes.data, e.ctypes.data, t.ctypes.data))
+        self.natoms_total, self.nlocal, self.stride = ntot, n, stride
+        self._keep = (nn, nb, dp, ty)
+        return f, e, float(t[0])
+
     def synchronize(self):
         self._c(self._L.snapgpu_synchronize(self._h))
 
@@ -360,12 +383,9 @@ def run_pipeline(problem, device=0, stage_timing=False) -> PipelineResult:
     """run_pipeline (pipeline.hpp:206-303) for the fused adjoint path on the GPU."""
     p = Problem.from_any(problem)
     with SnapEngine.for_problem(p, device) as eng:
-        eng.set_problem(p)
         if stage_timing:
             eng.enable_stage_timing(True)
-        eng.run()
-        f = eng.forces()
-        e, t = eng.energy()
+        f, e, t = eng.step(p.numneigh, p.nbr, p.disp, p.types)
         st = eng.stage_times() if stage_timing else None
     return PipelineResult(forces=f, eatom=e, etotal=t, stage_ms=st)
 

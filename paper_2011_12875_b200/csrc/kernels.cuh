@@ -88,7 +88,21 @@ struct PairArgs {
   const double* disp;     // nlocal*stride*3
   const int* types;       // natoms_total or null
   const double* weights;  // per type
+  int natoms_total, nweights;
+  double rc2;             // rcut^2
+  unsigned* err;          // validation flags (kErr*), set by k_compute_U
 };
+
+// Problem::validate (snap_core.hpp:89-118) restated on the device: the
+// U kernel checks every pair it reads and ORs these flags; later kernels
+// skip all work (and every scatter write) once a flag is set.
+enum : unsigned {
+  kErrCount = 1u, kErrIndex = 2u, kErrSelf = 4u, kErrZero = 8u, kErrCut = 16u, kErrType = 32u
+};
+
+__device__ __forceinline__ bool pipeline_failed(const PairArgs& A) {
+  return *(volatile const unsigned*)A.err != 0u;
+}
 
 // ---------------------------------------------------------------------------
 // per-pair geometry: map_to_3sphere (angular_basis.hpp:102-139),
@@ -239,9 +253,20 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32)
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * C::WARPS + w;
+  if (A.pr.types) {  // type range of every atom (grid-strided)
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < A.pr.natoms_total;
+         a += gridDim.x * blockDim.x) {
+      const int ty = A.pr.types[a];
+      if (ty < 0 || ty >= A.pr.nweights) atomicOr(A.pr.err, kErrType);
+    }
+  }
   if (i >= A.pr.nlocal) return;  // whole warp
   const int S = A.pr.stride;
-  const int nn = A.pr.numneigh[i];
+  int nn = A.pr.numneigh[i];
+  if (nn < 0 || nn > S) {
+    if (lane == 0) atomicOr(A.pr.err, kErrCount);
+    nn = 0;
+  }
   // shared: per warp geometry [S][5], then (T > 8) accumulators [2*NACC][32]
   double* geo = smem + (size_t)w * S * 5;
   double* accs = smem + (size_t)C::WARPS * S * 5 + (size_t)w * 2 * C::NACC * 32;
@@ -249,8 +274,21 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32)
   for (int k = lane; k < nn; k += 32) {
     const size_t pk = (size_t)i * S + k;
     const double* d = A.pr.disp + pk * 3;
+    const int j = A.pr.nbr[pk];
+    const double rsq = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+    unsigned bad = 0u;
+    if (j < 0 || j >= A.pr.natoms_total) bad |= kErrIndex;
+    if (j == A.pr.atom_lo + i) bad |= kErrSelf;
+    if (!(rsq > 0.0)) bad |= kErrZero;
+    if (!(rsq < A.pr.rc2)) bad |= kErrCut;
+    double wj = 0.0;
+    if (!(bad & kErrIndex)) {
+      const int ty = A.pr.types ? A.pr.types[j] : 0;
+      if (ty >= 0 && ty < A.pr.nweights) wj = A.pr.weights[ty];
+    }
+    if (bad) atomicOr(A.pr.err, bad);
     PairGeo g;
-    pair_geometry<false>(d[0], d[1], d[2], neighbor_weight(A.pr, A.pr.nbr[pk]), A.gp, g);
+    pair_geometry<false>(d[0], d[1], d[2], wj, A.gp, g);
     geo[k * 5 + 0] = g.ar;
     geo[k * 5 + 1] = g.ai;
     geo[k * 5 + 2] = g.br;
@@ -872,6 +910,7 @@ template <int T>
 __global__ void __launch_bounds__(DECfg<T>::WARPS * 32, (T <= 8 ? 2 : 3))
     k_fused_dE(const DEArgs A) {
   using C = DECfg<T>;
+  if (pipeline_failed(A.pr)) return;
   constexpr int NDIR = C::NDIR;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int r = lane % C::G, q = lane / C::G;
@@ -1082,6 +1121,7 @@ template <int T>
 __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
     k_fused_dE_rev(const DEArgs A) {
   using C = DERCfg<T>;
+  if (pipeline_failed(A.pr)) return;
   extern __shared__ double sbuf[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int r = lane % C::G, q = lane / C::G;
@@ -1311,7 +1351,7 @@ struct ScatterArgs {
 
 __global__ void __launch_bounds__(256) k_scatter_forces(const ScatterArgs A) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= A.nslots) return;
+  if (p >= A.nslots || pipeline_failed(A.pr)) return;
   const int S = A.pr.stride;
   const int i = p / S, k = p - i * S;
   if (k >= A.pr.numneigh[i]) return;

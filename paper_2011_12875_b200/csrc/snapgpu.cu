@@ -95,7 +95,6 @@ struct snapgpu_ctx {
   int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
 
   // problem shape
-  std::vector<int> h_numneigh;
   int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
   bool have_lists = false, have_U = false, have_Y = false, have_dE = false;
 
@@ -103,6 +102,8 @@ struct snapgpu_ctx {
   DevBuf<int> d_numneigh, d_nbr, d_types;
   DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal, d_part;
   DevBuf<unsigned> d_ticket;
+  DevBuf<unsigned> d_err;      // device validation flags (kErr*)
+  unsigned* h_err = nullptr;   // pinned readback of d_err
 
   // graph
   cudaGraph_t graph = nullptr;
@@ -183,6 +184,10 @@ PairArgs pair_args(const snapgpu_ctx* c) {
   p.disp = c->d_disp.p;
   p.types = c->d_types.p;
   p.weights = c->d_weights.p;
+  p.natoms_total = c->natoms_total;
+  p.nweights = static_cast<int>(c->weights.size());
+  p.rc2 = c->gp.rcut * c->gp.rcut;
+  p.err = c->d_err.p;
   return p;
 }
 
@@ -436,32 +441,26 @@ void need(bool ok, const char* what) {
   if (!ok) throw StateErr{std::string("stage called out of order: ") + what};
 }
 
+const char* device_error_message(unsigned f) {
+  if (f & kErrType) return "problem: atom type outside weight table";
+  if (f & kErrCount) return "problem: neighbor count outside stride";
+  if (f & kErrIndex) return "problem: neighbor index out of range";
+  if (f & kErrSelf) return "problem: self neighbor";
+  if (f & kErrZero) return "problem: zero-length neighbor displacement";
+  return "problem: neighbor at or beyond Rcut";
+}
+
+// host_validate = false defers Problem::validate to the U kernel's checks
+// (snapgpu_run_host reads the flags back with the results).
 void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int stride,
-               const int* numneigh, const int* nbr, const double* disp, const int* types) {
+               const int* numneigh, const int* nbr, const double* disp, const int* types,
+               bool host_validate = true) {
   require(natoms_total >= 0 && nlocal >= 0 && atom_lo >= 0 && atom_lo + nlocal <= natoms_total,
           "problem: owned range outside the atom count");
   require(nlocal == 0 || natoms_total > 0, "problem: no atoms");
   require(stride >= 0, "problem: negative neighbor stride");
   require(nlocal == 0 || stride == 0 || (numneigh && nbr && disp), "problem: null neighbor arrays");
-  const double rc2 = c->gp.rcut * c->gp.rcut;
-  const int nw = static_cast<int>(c->weights.size());
-  if (types)
-    for (int a = 0; a < natoms_total; ++a)
-      require(types[a] >= 0 && types[a] < nw, "problem: atom type outside weight table");
-  // Problem::validate (snap_core.hpp:89-118)
-  for (int i = 0; i < nlocal; ++i) {
-    require(numneigh[i] >= 0 && numneigh[i] <= stride, "problem: neighbor count outside stride");
-    for (int k = 0; k < numneigh[i]; ++k) {
-      const size_t pk = (size_t)i * stride + k;
-      const int j = nbr[pk];
-      require(j >= 0 && j < natoms_total, "problem: neighbor index out of range");
-      require(j != atom_lo + i, "problem: self neighbor");
-      const double* d = disp + pk * 3;
-      const double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
-      require(r2 > 0.0, "problem: zero-length neighbor displacement");
-      require(r2 < rc2, "problem: neighbor at or beyond Rcut");
-    }
-  }
+  c->have_lists = c->have_U = c->have_Y = c->have_dE = false;
   const bool reshape = natoms_total != c->natoms_total || nlocal != c->nlocal ||
                        stride != c->stride || atom_lo != c->atom_lo ||
                        (types != nullptr) != (c->d_types.p != nullptr);
@@ -500,6 +499,9 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
     c->ntiles = ntiles;
     plan_y(c);
   }
+  // Enqueue the uploads first (asynchronous from pinned memory) and validate
+  // on the host while they are in flight; a failed validation leaves the
+  // context without lists, so nothing runs on the uploaded data.
   if (nlocal > 0) {
     CK(cudaMemcpyAsync(c->d_numneigh.p, numneigh, sizeof(int) * nlocal, cudaMemcpyHostToDevice,
                        c->stream));
@@ -513,9 +515,37 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
   if (types)
     CK(cudaMemcpyAsync(c->d_types.p, types, sizeof(int) * natoms_total, cudaMemcpyHostToDevice,
                        c->stream));
-  c->h_numneigh.assign(numneigh, numneigh + nlocal);
+  if (!host_validate) {
+    c->have_lists = true;
+    return;
+  }
+  // Problem::validate (snap_core.hpp:89-118)
+  const double rc2 = c->gp.rcut * c->gp.rcut;
+  const int nw = static_cast<int>(c->weights.size());
+  if (types)
+    for (int a = 0; a < natoms_total; ++a)
+      require(types[a] >= 0 && types[a] < nw, "problem: atom type outside weight table");
+  for (int i = 0; i < nlocal; ++i) {
+    const int nn = numneigh[i];
+    require(nn >= 0 && nn <= stride, "problem: neighbor count outside stride");
+    const int* ip = nbr + (size_t)i * stride;
+    const double* dp = disp + (size_t)i * stride * 3;
+    bool idx_ok = true, self_ok = true, pos_ok = true, cut_ok = true;
+    for (int k = 0; k < nn; ++k) {
+      const int j = ip[k];
+      idx_ok &= (j >= 0) & (j < natoms_total);
+      self_ok &= (j != atom_lo + i);
+      const double r2 = dp[3 * k] * dp[3 * k] + dp[3 * k + 1] * dp[3 * k + 1] +
+                        dp[3 * k + 2] * dp[3 * k + 2];
+      pos_ok &= r2 > 0.0;
+      cut_ok &= r2 < rc2;
+    }
+    require(idx_ok, "problem: neighbor index out of range");
+    require(self_ok, "problem: self neighbor");
+    require(pos_ok, "problem: zero-length neighbor displacement");
+    require(cut_ok, "problem: neighbor at or beyond Rcut");
+  }
   c->have_lists = true;
-  c->have_U = c->have_Y = c->have_dE = false;
 }
 
 void record(snapgpu_ctx* c, int k) {
@@ -578,6 +608,10 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     c = new snapgpu_ctx();
     c->device = device;
     c->T = twojmax;
+    c->d_err.alloc(1);
+    CK(cudaMemset(c->d_err.p, 0, sizeof(unsigned)));
+    CK(cudaMallocHost(&c->h_err, sizeof(unsigned)));
+    *c->h_err = 0u;
     c->maps = IndexMaps::build(twojmax);
     require(nbeta == static_cast<int>(c->maps.triples.size()) && beta,
             "problem: beta length must match the triple count");
@@ -667,6 +701,8 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_etotal.release();
   c->d_part.release();
   c->d_ticket.release();
+  c->d_err.release();
+  if (c->h_err) cudaFreeHost(c->h_err);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return SNAPGPU_OK;
@@ -779,6 +815,39 @@ int snapgpu_run(snapgpu_ctx* c) {
   });
 }
 
+int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int stride,
+                     const int* numneigh, const int* nbr, const double* disp,
+                     const int* types, double* forces, double* eatom, double* etotal) {
+  if (!c) return SNAPGPU_EINVAL;
+  const int rc = guarded(c, [&] {
+    set_lists(c, natoms_total, atom_lo, nlocal, stride, numneigh, nbr, disp, types, false);
+  });
+  if (rc != SNAPGPU_OK) return rc;
+  const int rr = snapgpu_run(c);
+  if (rr != SNAPGPU_OK) return rr;
+  return guarded(c, [&] {
+    CK(cudaMemcpyAsync(c->h_err, c->d_err.p, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                       c->stream));
+    if (forces)
+      CK(cudaMemcpyAsync(forces, c->d_forces.p, sizeof(double) * 3 * c->natoms_total,
+                         cudaMemcpyDeviceToHost, c->stream));
+    if (eatom && c->nlocal > 0)
+      CK(cudaMemcpyAsync(eatom, c->d_eatom.p, sizeof(double) * c->nlocal, cudaMemcpyDeviceToHost,
+                         c->stream));
+    if (etotal)
+      CK(cudaMemcpyAsync(etotal, c->d_etotal.p, sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (*c->h_err) {
+      const unsigned f = *c->h_err;
+      CK(cudaMemsetAsync(c->d_err.p, 0, sizeof(unsigned), c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      c->have_lists = c->have_U = c->have_Y = c->have_dE = false;
+      throw InvalidArg{device_error_message(f)};
+    }
+  });
+}
+
 int snapgpu_synchronize(snapgpu_ctx* c) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
@@ -878,14 +947,17 @@ int snapgpu_get_dedr(snapgpu_ctx* c, double* out) {
     need(c->have_dE, "get_dedr before the force pass");
     const size_t n = (size_t)c->nlocal * c->stride * 3;
     std::vector<double> h(n);
+    std::vector<int> nnh(c->nlocal);
     if (n) {
       CK(cudaMemcpyAsync(h.data(), c->d_dedr.p, n * sizeof(double), cudaMemcpyDeviceToHost,
                          c->stream));
+      CK(cudaMemcpyAsync(nnh.data(), c->d_numneigh.p, sizeof(int) * c->nlocal,
+                         cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
     }
     // zero the unused (padding) slots like the reference's zero-filled dElist
     for (int i = 0; i < c->nlocal; ++i) {
-      const int nn = c->h_numneigh[i];
+      const int nn = nnh[i];
       for (int k = 0; k < c->stride; ++k)
         for (int d = 0; d < 3; ++d) {
           const size_t s = ((size_t)i * c->stride + k) * 3 + d;

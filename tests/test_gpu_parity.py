@@ -175,6 +175,37 @@ def test_errors_map_to_reference_exceptions(snap):
     eng.close()
 
 
+@pytest.mark.parametrize("case", ["cut", "self", "index", "zero", "count", "type"])
+def test_one_call_step_validates_on_device(snap, case):
+    """snapgpu_run_host defers Problem::validate (snap_core.hpp:89-118) to the
+    U kernel: every violation still raises InvalidArgument with the host
+    message, nothing is scattered, and the next valid step is exact."""
+    p = snap.bcc_problem(3, 3, 3, twojmax=8)
+    ref = snap.run_pipeline(p)
+    nn, nbr, disp = p.numneigh.copy(), p.nbr.copy(), p.disp.copy()
+    types = np.zeros(p.natoms, np.int32)
+    match = {"cut": "Rcut", "self": "self", "index": "index", "zero": "zero-length",
+             "count": "count", "type": "type"}[case]
+    if case == "cut":
+        disp[3, 2] = [5.0, 0.0, 0.0]
+    elif case == "self":
+        nbr[4, 1] = 4
+    elif case == "index":
+        nbr[5, 0] = p.natoms
+    elif case == "zero":
+        disp[6, 0] = 0.0
+    elif case == "count":
+        nn[7] = nbr.shape[1] + 1
+    else:
+        types[8] = 3
+    with snap.SnapEngine.for_problem(p) as eng:
+        with pytest.raises(snap.InvalidArgument, match=match):
+            eng.step(nn, nbr, disp, types)
+        f, e, t = eng.step(p.numneigh, p.nbr, p.disp)
+        assert normerr(f, ref.forces) <= 1e-13  # atomic scatter order varies
+        assert t == ref.etotal  # the energy reduction is deterministic
+
+
 def test_empty_and_isolated_atoms(snap, port):
     p = port.make_cluster(6, 8, 77)
     p.numneigh = p.numneigh.copy()
