@@ -1,0 +1,159 @@
+// ctx.hpp -- the engine context, shared by the host translation unit
+// (snapgpu.cu: C-ABI, planning, graph) and the per-twojmax kernel units
+// (launch_t.cu compiled once per 2J, so the build runs in parallel).
+// Internal header: not part of the C-ABI (include/snapgpu.h).
+//
+// A context mirrors the reference's DescriptorState (snap_core.hpp:130-172):
+// it owns every per-atom array, here in HBM, plus the host-built tables
+// (tables.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/snapgpu.h"
+#include "kernels.cuh"
+#include "tables.hpp"
+
+namespace snapgpu {
+namespace host {
+
+struct CudaError {
+  std::string msg;
+};
+
+#define CK(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw ::snapgpu::host::CudaError{std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+struct InvalidArg {
+  std::string msg;
+};
+struct StateErr {
+  std::string msg;
+};
+
+inline void require(bool ok, const char* m) {
+  if (!ok) throw InvalidArg{m};
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) return;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace host
+}  // namespace snapgpu
+
+struct snapgpu_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // parameters (SnapParams, snap_core.hpp:48-57)
+  int T = 0;
+  snapgpu::GeoParams gp{};
+  std::vector<double> beta, weights;
+  snapgpu::IndexMaps maps;
+  std::vector<double> cg, hf, ywgt;
+
+  // device tables
+  snapgpu::host::DevBuf<double> d_weights, d_itw, d_cw, d_citw;
+  snapgpu::host::DevBuf<int4> d_items;
+  snapgpu::host::DevBuf<int> d_rowbeg, d_tasks, d_expand, d_rwbeg;
+  snapgpu::YPlan yplan;
+  snapgpu::YCoopPlan ycplan;
+  int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
+  int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
+  snapgpu::host::DevBuf<int4> d_witems;
+  int task_cap = 0;
+  int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
+  int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
+
+  // problem shape
+  int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
+  bool have_lists = false, have_U = false, have_Y = false, have_dE = false;
+
+  // device arrays
+  snapgpu::host::DevBuf<int> d_numneigh, d_nbr, d_types;
+  snapgpu::host::DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal, d_part;
+  snapgpu::host::DevBuf<unsigned> d_ticket;
+  snapgpu::host::DevBuf<unsigned> d_err;  // device validation flags (kErr*)
+  unsigned* h_err = nullptr;              // pinned readback of d_err
+
+  // graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_valid = false;
+
+  bool fuse_scatter = true;  // dE kernel scatters forces (reference `fused` variant)
+
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[5] = {};
+  float stage_ms[4] = {0, 0, 0, 0};
+};
+
+namespace snapgpu {
+namespace host {
+
+inline PairArgs pair_args(const snapgpu_ctx* c) {
+  PairArgs p;
+  p.nlocal = c->nlocal;
+  p.stride = c->stride;
+  p.atom_lo = c->atom_lo;
+  p.numneigh = c->d_numneigh.p;
+  p.nbr = c->d_nbr.p;
+  p.disp = c->d_disp.p;
+  p.types = c->d_types.p;
+  p.weights = c->d_weights.p;
+  p.natoms_total = c->natoms_total;
+  p.nweights = static_cast<int>(c->weights.size());
+  p.rc2 = c->gp.rcut * c->gp.rcut;
+  p.err = c->d_err.p;
+  return p;
+}
+
+inline EnergyOut energy_out(snapgpu_ctx* c) {
+  EnergyOut E;
+  E.eatom = c->d_eatom.p;
+  E.part_sums = c->d_part.p;
+  E.ticket = c->d_ticket.p;
+  E.etotal = c->d_etotal.p;
+  return E;
+}
+
+// Per-2J launchers, explicitly instantiated in launch_t.cu (one object file
+// per 2J).  upload_cwin_t fills that object's own constant bank.
+template <int T> void launch_U_t(snapgpu_ctx* c);
+template <int T> void launch_Y_t(snapgpu_ctx* c);
+template <int T> void launch_DE_t(snapgpu_ctx* c);
+template <int T> void upload_cwin_t(int device, const YPlan& p);
+
+}  // namespace host
+}  // namespace snapgpu

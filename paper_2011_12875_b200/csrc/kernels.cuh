@@ -1338,6 +1338,7 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
   }
 }
 
+#ifndef SNAP_T  // non-template kernels: host translation unit only
 // ===========================================================================
 // scatter_forces (snap_core.hpp:872-953, concurrent-RMW strategy):
 // F_i += dE(i,k), F_{nbr} -= dE(i,k) with FP64 RED atomics.
@@ -1397,5 +1398,7 @@ __global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters, doubl
   for (int q = 0; q < 8; ++q) r += a[q];
   if (r == 1234.5678) out[0] = r;  // keep the chains alive
 }
+
+#endif  // SNAP_T
 
 }  // namespace snapgpu

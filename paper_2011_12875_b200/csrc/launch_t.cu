@@ -1,0 +1,147 @@
+// launch_t.cu -- kernel launches for ONE band limit 2J = SNAP_T.
+//
+// Compiled once per 2J (Makefile: -DSNAP_T=0..14) so the sm_100a kernels of
+// the different band limits build in parallel; snapgpu.cu dispatches on the
+// context's twojmax to the instantiations below.
+#include "ctx.hpp"
+
+#ifndef SNAP_T
+#error "compile with -DSNAP_T=<twojmax>"
+#endif
+
+namespace snapgpu {
+namespace host {
+
+template <int T>
+void launch_U_t(snapgpu_ctx* c) {
+  using C = UCfg<T>;
+  UArgs a;
+  a.pr = pair_args(c);
+  a.gp = c->gp;
+  a.V = c->d_V.p;
+  const size_t smem = sizeof(double) * ((size_t)C::WARPS * c->stride * 5 +
+                                        (C::REGACC ? 0 : (size_t)C::WARPS * 2 * C::NACC * 32));
+  static bool attr = false;
+  if (!attr || smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_compute_U<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)std::max<size_t>(smem, 48 * 1024)));
+    attr = true;
+  }
+  const int blocks = (c->nlocal + C::WARPS - 1) / C::WARPS;
+  k_compute_U<T><<<blocks, C::WARPS * 32, smem, c->stream>>>(a);
+  CK(cudaGetLastError());
+}
+
+template <int T, int TA>
+static void launch_Y_window(snapgpu_ctx* c) {
+  constexpr int NH = c_half_off(T + 1);
+  YArgs a;
+  a.V = c->d_V.p;
+  a.Y = c->d_Y.p;
+  a.items = c->d_items.p;
+  a.itw = c->d_itw.p;
+  a.row_begin = c->d_rowbeg.p;
+  a.cw = c->d_cw.p;
+  a.tasks = c->d_tasks.p;
+  a.task_cap = c->task_cap;
+  a.nlocal = c->nlocal;
+  a.E = energy_out(c);
+  const size_t smem = sizeof(double) * (2 * NH * TA + (size_t)c->y_warps * (T + 1) * 2 * 32);
+  CK(cudaFuncSetAttribute(k_compute_Y<T, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  dim3 grid((c->ntiles * 32) / TA, c->y_parts_used);
+  k_compute_Y<T, TA><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+  CK(cudaGetLastError());
+}
+
+template <int T>
+void launch_Y_t(snapgpu_ctx* c) {
+  constexpr int NH = c_half_off(T + 1);
+  if constexpr (cw_base(T) >= 0) {
+    if (c->y_impl == 0) {
+      constexpr int NF = c_full_off(T + 1);
+      constexpr int NP = NF + 2 * kXPad;
+      YWArgs a;
+      a.V = c->d_V.p;
+      a.Y = c->d_Y.p;
+      a.expand = c->d_expand.p;
+      a.items = c->d_witems.p;
+      a.itw = c->d_citw.p;
+      a.rw_begin = c->d_rwbeg.p;
+      a.nwarps = c->ycplan.warps;
+      a.tasks = c->d_tasks.p;
+      a.task_cap = c->task_cap;
+      a.nlocal = c->nlocal;
+      a.E = energy_out(c);
+      const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)c->y_warps * (T + 1) * 2 * 32);
+      CK(cudaFuncSetAttribute(k_compute_Y_cwin<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+      dim3 grid(c->ntiles, c->y_parts_used);
+      k_compute_Y_cwin<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
+  constexpr int RED = 8 * (T + 1) * 2 * 32 * 8;
+  if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
+    if (c->y_ta == 32) return launch_Y_window<T, 32>(c);
+  }
+  if constexpr (2 * NH * 16 * 8 + RED <= 200 * 1024) {
+    if (c->y_ta >= 16) return launch_Y_window<T, 16>(c);
+  }
+  return launch_Y_window<T, 8>(c);
+}
+
+template <int T>
+void launch_DE_t(snapgpu_ctx* c) {
+  using C = DECfg<T>;
+  DEArgs a;
+  a.pr = pair_args(c);
+  a.gp = c->gp;
+  a.Y = c->d_Y.p;
+  a.dedr = c->d_dedr.p;
+  a.forces = c->fuse_scatter ? c->d_forces.p : nullptr;
+  a.nslots = c->nlocal * c->stride;
+  if (c->de_impl == 0) {  // reverse mode
+    using R = DERCfg<T>;
+    const int per_block = R::WARPS * R::PPW;
+    const int blocks = (a.nslots + per_block - 1) / per_block;
+    if (blocks > 0) {
+      CK(cudaFuncSetAttribute(k_fused_dE_rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              R::SMEM));
+      k_fused_dE_rev<T><<<blocks, R::WARPS * 32, R::SMEM, c->stream>>>(a);
+      CK(cudaGetLastError());
+    }
+    return;
+  }
+  const int per_block = C::WARPS * C::PPW;
+  const int blocks = (a.nslots + per_block - 1) / per_block;
+  if (blocks > 0) {
+    k_fused_dE<T><<<blocks, C::WARPS * 32, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+  }
+}
+
+// The windowed C' coefficients of the constant-window compute_Y live in this
+// object's constant bank (cCW, kernels.cuh), uploaded once per device.
+template <int T>
+void upload_cwin_t(int device, const YPlan& p) {
+  if constexpr (cw_base(T) >= 0) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int d : done)
+      if (d == device) return;
+    CK(cudaMemcpyToSymbol(cCW, p.cw.data(), p.cw.size() * sizeof(double),
+                          static_cast<size_t>(cw_base(T)) * sizeof(double)));
+    done.push_back(device);
+  }
+}
+
+template void launch_U_t<SNAP_T>(snapgpu_ctx*);
+template void launch_Y_t<SNAP_T>(snapgpu_ctx*);
+template void launch_DE_t<SNAP_T>(snapgpu_ctx*);
+template void upload_cwin_t<SNAP_T>(int, const YPlan&);
+
+}  // namespace host
+}  // namespace snapgpu

@@ -1,124 +1,17 @@
-// snapgpu.cu -- context, launches and the C-ABI (include/snapgpu.h).
-//
-// A context mirrors the reference's DescriptorState (snap_core.hpp:130-172):
-// it owns every per-atom array, here in HBM, plus the host-built tables
-// (tables.cpp).  Stage entry points launch the kernels of kernels.cuh on the
-// context stream; snapgpu_run replays the whole force step from a CUDA graph.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
+// snapgpu.cu -- context lifetime, planning, stage sequencing, CUDA graph and
+// the C-ABI (include/snapgpu.h).  The kernels are launched from the per-2J
+// objects built from launch_t.cu; snapgpu_run replays the whole force step
+// from a CUDA graph.
 #include <cstdarg>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <mutex>
-#include <string>
-#include <vector>
 
-#include "../../include/snapgpu.h"
-#include "kernels.cuh"
-#include "tables.hpp"
+#include "ctx.hpp"
 
 using namespace snapgpu;
+using namespace snapgpu::host;
 
 namespace {
 
 thread_local std::string g_err = "";
-
-struct CudaError {
-  std::string msg;
-};
-
-#define CK(expr)                                                                        \
-  do {                                                                                  \
-    cudaError_t _e = (expr);                                                            \
-    if (_e != cudaSuccess)                                                              \
-      throw CudaError{std::string(#expr) + ": " + cudaGetErrorString(_e)};              \
-  } while (0)
-
-struct InvalidArg {
-  std::string msg;
-};
-struct StateErr {
-  std::string msg;
-};
-
-inline void require(bool ok, const char* m) {
-  if (!ok) throw InvalidArg{m};
-}
-
-template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  void alloc(size_t count) {
-    if (count <= n && p) return;
-    release();
-    if (count == 0) return;
-    CK(cudaMalloc(&p, count * sizeof(T)));
-    n = count;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-};
-
-}  // namespace
-
-struct snapgpu_ctx {
-  int device = 0;
-  cudaStream_t own_stream = nullptr;
-  cudaStream_t stream = nullptr;
-  std::string err;
-
-  // parameters (SnapParams, snap_core.hpp:48-57)
-  int T = 0;
-  GeoParams gp{};
-  std::vector<double> beta, weights;
-  IndexMaps maps;
-  std::vector<double> cg, hf, ywgt;
-
-  // device tables
-  DevBuf<double> d_weights, d_itw, d_cw, d_citw;
-  DevBuf<int4> d_items;
-  DevBuf<int> d_rowbeg, d_tasks, d_expand, d_rwbeg;
-  YPlan yplan;
-  YCoopPlan ycplan;
-  int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
-  int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
-  DevBuf<int4> d_witems;
-  int task_cap = 0;
-  int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
-  int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
-
-  // problem shape
-  int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
-  bool have_lists = false, have_U = false, have_Y = false, have_dE = false;
-
-  // device arrays
-  DevBuf<int> d_numneigh, d_nbr, d_types;
-  DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal, d_part;
-  DevBuf<unsigned> d_ticket;
-  DevBuf<unsigned> d_err;      // device validation flags (kErr*)
-  unsigned* h_err = nullptr;   // pinned readback of d_err
-
-  // graph
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  bool graph_valid = false;
-
-  bool fuse_scatter = true;  // dE kernel scatters forces (reference `fused` variant)
-
-  // timing
-  bool timing = false;
-  cudaEvent_t ev[5] = {};
-  float stage_ms[4] = {0, 0, 0, 0};
-};
-
-namespace {
 
 void invalidate_graph(snapgpu_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -152,168 +45,26 @@ int guarded(snapgpu_ctx* c, F&& f) {
 // ---------------------------------------------------------------------------
 // template dispatch over twojmax
 // ---------------------------------------------------------------------------
-template <template <int> class F, class... Args>
-void dispatch_T(int T, Args&&... args) {
-  switch (T) {
-    case 0: F<0>::go(args...); break;
-    case 1: F<1>::go(args...); break;
-    case 2: F<2>::go(args...); break;
-    case 3: F<3>::go(args...); break;
-    case 4: F<4>::go(args...); break;
-    case 5: F<5>::go(args...); break;
-    case 6: F<6>::go(args...); break;
-    case 7: F<7>::go(args...); break;
-    case 8: F<8>::go(args...); break;
-    case 9: F<9>::go(args...); break;
-    case 10: F<10>::go(args...); break;
-    case 11: F<11>::go(args...); break;
-    case 12: F<12>::go(args...); break;
-    case 13: F<13>::go(args...); break;
-    case 14: F<14>::go(args...); break;
-    default: throw InvalidArg{"twojmax outside [0, 14]"};
-  }
+template <class Fn>
+Fn pick_T(int T, Fn f0, Fn f1, Fn f2, Fn f3, Fn f4, Fn f5, Fn f6, Fn f7, Fn f8, Fn f9,
+          Fn f10, Fn f11, Fn f12, Fn f13, Fn f14) {
+  const Fn tab[15] = {f0, f1, f2, f3, f4, f5, f6, f7, f8, f9, f10, f11, f12, f13, f14};
+  if (T < 0 || T > 14) throw InvalidArg{"twojmax outside [0, 14]"};
+  return tab[T];
+}
+#define SNAP_PICK(name, T)                                                              \
+  pick_T<void (*)(snapgpu_ctx*)>(T, name<0>, name<1>, name<2>, name<3>, name<4>, name<5>, \
+                                 name<6>, name<7>, name<8>, name<9>, name<10>, name<11>, \
+                                 name<12>, name<13>, name<14>)
+
+void upload_cwin(int device, int T, const YPlan& p) {
+  using Fn = void (*)(int, const YPlan&);
+  pick_T<Fn>(T, upload_cwin_t<0>, upload_cwin_t<1>, upload_cwin_t<2>, upload_cwin_t<3>,
+             upload_cwin_t<4>, upload_cwin_t<5>, upload_cwin_t<6>, upload_cwin_t<7>,
+             upload_cwin_t<8>, upload_cwin_t<9>, upload_cwin_t<10>, upload_cwin_t<11>,
+             upload_cwin_t<12>, upload_cwin_t<13>, upload_cwin_t<14>)(device, p);
 }
 
-PairArgs pair_args(const snapgpu_ctx* c) {
-  PairArgs p;
-  p.nlocal = c->nlocal;
-  p.stride = c->stride;
-  p.atom_lo = c->atom_lo;
-  p.numneigh = c->d_numneigh.p;
-  p.nbr = c->d_nbr.p;
-  p.disp = c->d_disp.p;
-  p.types = c->d_types.p;
-  p.weights = c->d_weights.p;
-  p.natoms_total = c->natoms_total;
-  p.nweights = static_cast<int>(c->weights.size());
-  p.rc2 = c->gp.rcut * c->gp.rcut;
-  p.err = c->d_err.p;
-  return p;
-}
-
-template <int T>
-struct LaunchU {
-  static void go(snapgpu_ctx* c) {
-    using C = UCfg<T>;
-    UArgs a;
-    a.pr = pair_args(c);
-    a.gp = c->gp;
-    a.V = c->d_V.p;
-    const size_t smem = sizeof(double) * ((size_t)C::WARPS * c->stride * 5 +
-                                          (C::REGACC ? 0 : (size_t)C::WARPS * 2 * C::NACC * 32));
-    static bool attr = false;
-    if (!attr || smem > 48 * 1024) {
-      CK(cudaFuncSetAttribute(k_compute_U<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)std::max<size_t>(smem, 48 * 1024)));
-      attr = true;
-    }
-    const int blocks = (c->nlocal + C::WARPS - 1) / C::WARPS;
-    k_compute_U<T><<<blocks, C::WARPS * 32, smem, c->stream>>>(a);
-    CK(cudaGetLastError());
-  }
-};
-
-EnergyOut energy_out(snapgpu_ctx* c) {
-  EnergyOut E;
-  E.eatom = c->d_eatom.p;
-  E.part_sums = c->d_part.p;
-  E.ticket = c->d_ticket.p;
-  E.etotal = c->d_etotal.p;
-  return E;
-}
-
-template <int T>
-struct LaunchY {
-  template <int TA>
-  static void launch(snapgpu_ctx* c) {
-    constexpr int NH = c_half_off(T + 1);
-    YArgs a;
-    a.V = c->d_V.p;
-    a.Y = c->d_Y.p;
-    a.items = c->d_items.p;
-    a.itw = c->d_itw.p;
-    a.row_begin = c->d_rowbeg.p;
-    a.cw = c->d_cw.p;
-    a.tasks = c->d_tasks.p;
-    a.task_cap = c->task_cap;
-    a.nlocal = c->nlocal;
-    a.E = energy_out(c);
-    const size_t smem = sizeof(double) * (2 * NH * TA + (size_t)c->y_warps * (T + 1) * 2 * 32);
-    CK(cudaFuncSetAttribute(k_compute_Y<T, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    dim3 grid((c->ntiles * 32) / TA, c->y_parts_used);
-    k_compute_Y<T, TA><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
-    CK(cudaGetLastError());
-  }
-  static void go(snapgpu_ctx* c) {
-    constexpr int NH = c_half_off(T + 1);
-    if constexpr (cw_base(T) >= 0) {
-      if (c->y_impl == 0) {
-        constexpr int NF = c_full_off(T + 1);
-        constexpr int NP = NF + 2 * kXPad;
-        YWArgs a;
-        a.V = c->d_V.p;
-        a.Y = c->d_Y.p;
-        a.expand = c->d_expand.p;
-        a.items = c->d_witems.p;
-        a.itw = c->d_citw.p;
-        a.rw_begin = c->d_rwbeg.p;
-        a.nwarps = c->ycplan.warps;
-        a.tasks = c->d_tasks.p;
-        a.task_cap = c->task_cap;
-        a.nlocal = c->nlocal;
-        a.E = energy_out(c);
-        const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)c->y_warps * (T + 1) * 2 * 32);
-        CK(cudaFuncSetAttribute(k_compute_Y_cwin<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-        dim3 grid(c->ntiles, c->y_parts_used);
-        k_compute_Y_cwin<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
-        CK(cudaGetLastError());
-        return;
-      }
-    }
-    constexpr int RED = 8 * (T + 1) * 2 * 32 * 8;
-    if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
-      if (c->y_ta == 32) return launch<32>(c);
-    }
-    if constexpr (2 * NH * 16 * 8 + RED <= 200 * 1024) {
-      if (c->y_ta >= 16) return launch<16>(c);
-    }
-    return launch<8>(c);
-  }
-};
-
-template <int T>
-struct LaunchDE {
-  static void go(snapgpu_ctx* c) {
-    using C = DECfg<T>;
-    DEArgs a;
-    a.pr = pair_args(c);
-    a.gp = c->gp;
-    a.Y = c->d_Y.p;
-    a.dedr = c->d_dedr.p;
-    a.forces = c->fuse_scatter ? c->d_forces.p : nullptr;
-    a.nslots = c->nlocal * c->stride;
-    if (c->de_impl == 0) {  // reverse mode
-      using R = DERCfg<T>;
-      const int per_block = R::WARPS * R::PPW;
-      const int blocks = (a.nslots + per_block - 1) / per_block;
-      if (blocks > 0) {
-        CK(cudaFuncSetAttribute(k_fused_dE_rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                R::SMEM));
-        k_fused_dE_rev<T><<<blocks, R::WARPS * 32, R::SMEM, c->stream>>>(a);
-        CK(cudaGetLastError());
-      }
-      return;
-    }
-    const int per_block = C::WARPS * C::PPW;
-    const int blocks = (a.nslots + per_block - 1) / per_block;
-    if (blocks > 0) {
-      k_fused_dE<T><<<blocks, C::WARPS * 32, 0, c->stream>>>(a);
-      CK(cudaGetLastError());
-    }
-  }
-};
 
 // compute_Y work split: TA atoms per CTA (32 when the V tile fits, smaller
 // tiles for small problems so the SMs fill), W warps per CTA owning target
@@ -390,25 +141,14 @@ void build_ycoop(snapgpu_ctx* c) {
   upload_beta(c);
 }
 
-void upload_cwin(int device, int T, const YPlan& p) {
-  static std::mutex mu;
-  static std::vector<std::pair<int, int>> done;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& d : done)
-    if (d.first == device && d.second == T) return;
-  CK(cudaMemcpyToSymbol(cCW, p.cw.data(), p.cw.size() * sizeof(double),
-                        static_cast<size_t>(cw_base(T)) * sizeof(double)));
-  done.push_back({device, T});
-}
-
 
 void launch_U(snapgpu_ctx* c) {
-  if (c->nlocal > 0) dispatch_T<LaunchU>(c->T, c);
+  if (c->nlocal > 0) SNAP_PICK(launch_U_t, c->T)(c);
 }
 void launch_Y(snapgpu_ctx* c) {
   CK(cudaMemsetAsync(c->d_eatom.p, 0, sizeof(double) * std::max(1, c->nlocal), c->stream));
   if (c->nlocal > 0) {
-    dispatch_T<LaunchY>(c->T, c);  // energy total in the kernel's last CTA
+    SNAP_PICK(launch_Y_t, c->T)(c);  // energy total in the kernel's last CTA
   } else {
     CK(cudaMemsetAsync(c->d_etotal.p, 0, sizeof(double), c->stream));
   }
@@ -421,7 +161,7 @@ void launch_dE(snapgpu_ctx* c) {
   if (c->fuse_scatter)
     CK(cudaMemsetAsync(c->d_forces.p, 0, sizeof(double) * 3 * std::max(1, c->natoms_total),
                        c->stream));
-  if (c->nlocal > 0) dispatch_T<LaunchDE>(c->T, c);
+  if (c->nlocal > 0) SNAP_PICK(launch_DE_t, c->T)(c);
 }
 void launch_scatter(snapgpu_ctx* c) {
   CK(cudaMemsetAsync(c->d_forces.p, 0, sizeof(double) * 3 * std::max(1, c->natoms_total),
