@@ -34,7 +34,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libsnapgpu.so")
+LIB_PATH = os.environ.get("SNAPGPU_LIB") or os.path.join(_HERE, "_build", "libsnapgpu.so")  # env: A/B builds (development)
 
 
 class InvalidArgument(ValueError):

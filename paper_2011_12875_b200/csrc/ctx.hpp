@@ -85,12 +85,11 @@ struct snapgpu_ctx {
   // device tables
   snapgpu::host::DevBuf<double> d_weights, d_itw, d_cw, d_citw;
   snapgpu::host::DevBuf<int4> d_items;
-  snapgpu::host::DevBuf<int> d_rowbeg, d_tasks, d_expand, d_rwbeg;
+  snapgpu::host::DevBuf<int> d_rowbeg, d_tasks, d_expand;
   snapgpu::YPlan yplan;
   snapgpu::YCoopPlan ycplan;
   int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
   int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
-  snapgpu::host::DevBuf<int4> d_witems;
   int task_cap = 0;
   int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
   int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
@@ -149,11 +148,16 @@ inline EnergyOut energy_out(snapgpu_ctx* c) {
 }
 
 // Per-2J launchers, explicitly instantiated in launch_t.cu (one object file
-// per 2J).  upload_cwin_t fills that object's own constant bank.
+// per 2J).  upload_ytables_t fills that object's own constant bank.
 template <int T> void launch_U_t(snapgpu_ctx* c);
 template <int T> void launch_Y_t(snapgpu_ctx* c);
 template <int T> void launch_DE_t(snapgpu_ctx* c);
-template <int T> void upload_cwin_t(int device, const YPlan& p);
+struct YTablesHost {  // constant-bank tables of k_compute_Y_cwin (kernels.cuh)
+  std::vector<double> cw;
+  std::vector<uint4> items;
+  std::vector<int> rw_begin;
+};
+template <int T> void upload_ytables_t(int device, const YTablesHost& t);
 
 }  // namespace host
 }  // namespace snapgpu

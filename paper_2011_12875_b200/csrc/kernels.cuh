@@ -194,6 +194,9 @@ __host__ __device__ constexpr double mirror_R(int t) {
 // memory (T > 8); one cross-slot shuffle reduction at the end, then the
 // atom's V row is written once: no global atomics.
 // ===========================================================================
+#ifndef SNAP_U_MINB
+#define SNAP_U_MINB 1
+#endif
 struct UArgs {
   PairArgs pr;
   GeoParams gp;
@@ -247,7 +250,7 @@ struct UAcc<T, false> {  // lane-private slots: [q][re|im][32]
 };
 
 template <int T>
-__global__ void __launch_bounds__(UCfg<T>::WARPS * 32)
+__global__ void __launch_bounds__(UCfg<T>::WARPS * 32, SNAP_U_MINB)
     k_compute_U(const UArgs A) {
   using C = UCfg<T>;
   extern __shared__ double smem[];
@@ -688,26 +691,168 @@ __host__ __device__ constexpr int cw_base(int T) {  // windowed C' of 2J = 0..8 
   for (int s = 0; s < T; ++s) o += c_cw_total(s);
   return o;
 }
-constexpr int kCwTotal = cw_base(8) + c_cw_total(8);
-__constant__ double cCW[kCwTotal];
-constexpr int kXPad = 16;  // zero elements before/after each X plane
+// X planes carry kXPad zero elements on each side: the window reads reach
+// kXPad >= J2 + 1 = 9 below the first row and D <= 8 above the last.
+constexpr int kXPad = 12;
+constexpr int kYWarps = 12;      // warps per k_compute_Y_cwin CTA
+constexpr int kYItemCap = 1536;  // row-pair units at 2J = 8: 838 (1479 items)
+#ifndef SNAP_Y_PAIR_U
+#define SNAP_Y_PAIR_U 2
+#endif
+constexpr int kYPairU = SNAP_Y_PAIR_U;  // window block length of the paired loop
+
+// beta-independent tables of the constant-window kernel, in the constant bank
+// of the per-2J object (launch_t.cu, uploaded once per device): warp-uniform
+// reads, so every access is a broadcast from the constant cache.
+//   cCW     windowed C' coefficients, rows of length j+1 per (tuple, a2)
+//   cYItems row-pair units {x1 window base (full idx + D) | x2 row base << 16,
+//           J2 | C' offset << 8, same x1|x2 of the second item, W index},
+//           grouped by target row, then by warp (pairs, then singles)
+//   cYRowW  [row][2*warp+kind] unit ranges
+#if defined(SNAP_T) && SNAP_T <= 8
+__constant__ double cCW[c_cw_total(SNAP_T)];
+__constant__ uint4 cYItems[kYItemCap];
+__constant__ int cYRowW[c_acc_off(SNAP_T + 1) * (2 * kYWarps + 1)];
+#endif
 
 struct YWArgs {
   const double* V;
   double* Y;
-  const int* expand;
-  const int4* items;    // {x1 window base (full idx + D), x2 row base, J2 | coff<<8, 0}
-  const double* itw;    // W per item
-  const int* rw_begin;  // [row][warp]
-  int nwarps;
+  const int* expand;    // half -> full scatter map (tables.cpp:half_scatter_map)
+  const double* itw;    // W per item (beta-dependent; staged into shared memory)
+  int nitems;
   const int* tasks;
   int task_cap;
   int nlocal;
   EnergyOut E;
 };
 
+#if defined(SNAP_T) && SNAP_T <= 8
+
+// G row-pair items (G = 1, or a pair of items sharing tuple and target row,
+// hence every C' coefficient) accumulated into the row outputs acc[ma]:
+//     acc[ma] += C'(a1, a2) * sum_g W_g x1_g[a1] x2_g[a2],  a1 = ma + D - a2
+// a2 runs over the x2 row; x1 lives in a register window E aligned with
+// the outputs: E[U-1+ma] = x1[ma + D - a2] (current window) and the U-1 slots
+// below hold the elements entering during a block of U steps, so step u of a
+// block reads E[U-1+ma-u] (compile-time index) and only one re-alignment per
+// block is needed.
+template <int G, int U, int L, int JW, int NP>
+__device__ __forceinline__ void yw_units(const double* __restrict__ sX,
+                                         const double* __restrict__ sW, int lane, int b, int e,
+                                         double (&ar)[L], double (&ai)[L]) {
+  for (int it = b; it < e; ++it) {
+    const uint4 m = cYItems[it];
+    const int J2 = m.y & 0xff;
+    const double* c0 = cCW + (m.y >> 8);
+    const double* p1[G];
+    const double* p2[G];
+    double wt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const unsigned xb = g == 0 ? m.x : m.z;
+      p1[g] = sX + (kXPad + (xb & 0xffff)) * 32 + lane;  // x1[base + k] at p1[k*32]
+      p2[g] = sX + (kXPad + (xb >> 16)) * 32 + lane;
+      wt[g] = sW[m.w + g];
+    }
+    double er[G][L + U - 1], ei[G][L + U - 1];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int ma = 0; ma < L; ++ma) {
+        er[g][U - 1 + ma] = p1[g][ma * 32];
+        ei[g][U - 1 + ma] = p1[g][(NP + ma) * 32];
+      }
+    int a2 = 0;
+    for (; a2 + U - 1 <= J2; a2 += U) {
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int k = 1; k < U; ++k) {  // x1[D - a2 - k]
+          er[g][U - 1 - k] = p1[g][(-a2 - k) * 32];
+          ei[g][U - 1 - k] = p1[g][(NP - a2 - k) * 32];
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double x2r[G], x2i[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          x2r[g] = wt[g] * p2[g][(a2 + u) * 32];
+          x2i[g] = wt[g] * p2[g][(NP + a2 + u) * 32];
+        }
+        const double* c = c0 + (a2 + u) * JW;
+#pragma unroll
+        for (int ma = 0; ma < L; ++ma) {
+          const double cc = c[ma];
+          double pr = er[0][U - 1 + ma - u] * x2r[0];
+          double pi = er[0][U - 1 + ma - u] * x2i[0];
+          pr = fma(-ei[0][U - 1 + ma - u], x2i[0], pr);
+          pi = fma(ei[0][U - 1 + ma - u], x2r[0], pi);
+#pragma unroll
+          for (int g = 1; g < G; ++g) {
+            pr = fma(er[g][U - 1 + ma - u], x2r[g], pr);
+            pi = fma(er[g][U - 1 + ma - u], x2i[g], pi);
+            pr = fma(-ei[g][U - 1 + ma - u], x2i[g], pr);
+            pi = fma(ei[g][U - 1 + ma - u], x2r[g], pi);
+          }
+          ar[ma] = fma(cc, pr, ar[ma]);
+          ai[ma] = fma(cc, pi, ai[ma]);
+        }
+      }
+      // re-align: new window = x1[ma + D - a2 - U] = E[ma - 1], E[-1] loaded
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int ma = L - 1; ma >= 1; --ma) {
+          er[g][U - 1 + ma] = er[g][ma - 1];
+          ei[g][U - 1 + ma] = ei[g][ma - 1];
+        }
+        er[g][U - 1] = p1[g][(-a2 - U) * 32];
+        ei[g][U - 1] = p1[g][(NP - a2 - U) * 32];
+      }
+    }
+    for (; a2 <= J2; ++a2) {  // remainder, one step at a time
+      double x2r[G], x2i[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        x2r[g] = wt[g] * p2[g][a2 * 32];
+        x2i[g] = wt[g] * p2[g][(NP + a2) * 32];
+      }
+      const double* c = c0 + a2 * JW;
+#pragma unroll
+      for (int ma = 0; ma < L; ++ma) {
+        const double cc = c[ma];
+        double pr = er[0][U - 1 + ma] * x2r[0];
+        double pi = er[0][U - 1 + ma] * x2i[0];
+        pr = fma(-ei[0][U - 1 + ma], x2i[0], pr);
+        pi = fma(ei[0][U - 1 + ma], x2r[0], pi);
+#pragma unroll
+        for (int g = 1; g < G; ++g) {
+          pr = fma(er[g][U - 1 + ma], x2r[g], pr);
+          pi = fma(er[g][U - 1 + ma], x2i[g], pi);
+          pr = fma(-ei[g][U - 1 + ma], x2i[g], pr);
+          pi = fma(ei[g][U - 1 + ma], x2r[g], pi);
+        }
+        ar[ma] = fma(cc, pr, ar[ma]);
+        ai[ma] = fma(cc, pi, ai[ma]);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int ma = L - 1; ma > 0; --ma) {
+          er[g][U - 1 + ma] = er[g][U - 2 + ma];
+          ei[g][U - 1 + ma] = ei[g][U - 2 + ma];
+        }
+        er[g][U - 1] = p1[g][(-a2 - 1) * 32];
+        ei[g][U - 1] = p1[g][(NP - a2 - 1) * 32];
+      }
+    }
+  }
+}
+
 template <int T, int J, bool MID>
 __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __restrict__ sred,
+                                       const double* __restrict__ sW,
                                        int lane, int w, int nw, int mb, int rid, const YWArgs& A,
                                        double* __restrict__ Yt, double& e_acc) {
   constexpr int NF = c_full_off(T + 1);
@@ -715,80 +860,12 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
   constexpr int NH = c_half_off(T + 1);
   constexpr int L = MID ? J / 2 + 1 : J + 1;
   constexpr int JW = J + 1;
-  constexpr int CWB = cw_base(T);
   double ar[L], ai[L];
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
-  const int* rb = A.rw_begin + rid * (A.nwarps + 1);
-  const int b = __ldg(rb + w), e = __ldg(rb + w + 1);
-  for (int it = b; it < e; ++it) {
-    const int4 m = __ldg(A.items + it);
-    const double wt = __ldg(A.itw + it);
-    const int J2 = m.z & 0xff;
-    const int coff = CWB + (m.z >> 8);
-    const double* p1 = sX + (kXPad + m.x) * 32 + lane;  // x1[m.x + k] at p1[k*32]
-    const double* p2 = sX + (kXPad + m.y) * 32 + lane;
-    // Register window E: E[U-1+ma] = x1[ma + D - a2] (current window); the
-    // U-1 slots below hold the elements entering during a block of U steps,
-    // so step u of a block reads E[U-1+ma-u] (compile-time index) and only
-    // one re-alignment per block is needed.
-    constexpr int U = 3;
-    double er[L + U - 1], ei[L + U - 1];
-#pragma unroll
-    for (int ma = 0; ma < L; ++ma) {
-      er[U - 1 + ma] = p1[ma * 32];
-      ei[U - 1 + ma] = p1[(NP + ma) * 32];
-    }
-    int a2 = 0;
-    for (; a2 + U - 1 <= J2; a2 += U) {
-#pragma unroll
-      for (int k = 1; k < U; ++k) {  // x1[D - a2 - k]
-        er[U - 1 - k] = p1[(-a2 - k) * 32];
-        ei[U - 1 - k] = p1[(NP - a2 - k) * 32];
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const double x2r = wt * p2[(a2 + u) * 32], x2i = wt * p2[(NP + a2 + u) * 32];
-        const double* c = cCW + coff + (a2 + u) * JW;
-#pragma unroll
-        for (int ma = 0; ma < L; ++ma) {
-          const double cc = c[ma];
-          const double wr = er[U - 1 + ma - u], wi = ei[U - 1 + ma - u];
-          const double pr = wr * x2r - wi * x2i;
-          const double pi = wr * x2i + wi * x2r;
-          ar[ma] = fma(cc, pr, ar[ma]);
-          ai[ma] = fma(cc, pi, ai[ma]);
-        }
-      }
-      // re-align: new window = x1[ma + D - a2 - U] = E[ma - 1], E[-1] loaded
-#pragma unroll
-      for (int ma = L - 1; ma >= 1; --ma) {
-        er[U - 1 + ma] = er[ma - 1];
-        ei[U - 1 + ma] = ei[ma - 1];
-      }
-      er[U - 1] = p1[(-a2 - U) * 32];
-      ei[U - 1] = p1[(NP - a2 - U) * 32];
-    }
-    for (; a2 <= J2; ++a2) {  // remainder, one step at a time
-      const double x2r = wt * p2[a2 * 32], x2i = wt * p2[(NP + a2) * 32];
-      const double* c = cCW + coff + a2 * JW;
-#pragma unroll
-      for (int ma = 0; ma < L; ++ma) {
-        const double cc = c[ma];
-        const double pr = er[U - 1 + ma] * x2r - ei[U - 1 + ma] * x2i;
-        const double pi = er[U - 1 + ma] * x2i + ei[U - 1 + ma] * x2r;
-        ar[ma] = fma(cc, pr, ar[ma]);
-        ai[ma] = fma(cc, pi, ai[ma]);
-      }
-#pragma unroll
-      for (int ma = L - 1; ma > 0; --ma) {
-        er[U - 1 + ma] = er[U - 2 + ma];
-        ei[U - 1 + ma] = ei[U - 2 + ma];
-      }
-      er[U - 1] = p1[(-a2 - 1) * 32];
-      ei[U - 1] = p1[(NP - a2 - 1) * 32];
-    }
-  }
+  const int* rb = cYRowW + rid * (2 * kYWarps + 1) + 2 * w;
+  yw_units<2, kYPairU, L, JW, NP>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
+  yw_units<1, 3, L, JW, NP>(sX, sW, lane, rb[1], rb[2], ar, ai);        // singles
 #pragma unroll
   for (int m = 0; m < L; ++m) {
     sred[((w * (T + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
@@ -815,32 +892,55 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
 }
 
 template <int T>
-__global__ void __launch_bounds__(384, 1) k_compute_Y_cwin(const YWArgs A) {
+__global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs A) {
   constexpr int NF = c_full_off(T + 1);
   constexpr int NP = NF + 2 * kXPad;
   constexpr int NH = c_half_off(T + 1);
   extern __shared__ double smem[];
   double* sX = smem;                  // [re|im][pad | full idx | pad][32]
   double* sred = smem + 2 * NP * 32;  // [warp][T+1][re|im][32]
-  __shared__ double se[12][32];
+  double* sW = sred + kYWarps * (T + 1) * 2 * 32;  // W per item
+  __shared__ double se[kYWarps][32];
+  for (int e = threadIdx.x; e < A.nitems; e += blockDim.x) sW[e] = __ldg(A.itw + e);
   const int tile = blockIdx.x;
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
   for (int e = threadIdx.x; e < kXPad * 32; e += blockDim.x) {
     sX[e] = sX[(kXPad + NF) * 32 + e] = 0.0;
     sX[NP * 32 + e] = sX[(NP + kXPad + NF) * 32 + e] = 0.0;
   }
-  for (int e = threadIdx.x; e < NF * 32; e += blockDim.x) {
-    const int f = e >> 5, ln = e & 31;
-    const int code = __ldg(A.expand + f);
-    const int src = code >> 2;
-    double re = Vt[src * 32 + ln], im = Vt[(NH + src) * 32 + ln];
-    if (code & 2) im = -im;
-    if (code & 1) {
-      re = -re;
-      im = -im;
+  {
+    // Half stack -> full mirrored X: warp w takes half elements h = w + nw k
+    // (one coalesced 256 B row per plane), writes it at its full position and,
+    // off the middle row, its mirror (t, t-mb, t-ma) = (-1)^(ma+mb) conj.
+    // All loads of a thread are issued before any store (no dependent
+    // table -> data round trips).
+    constexpr int KH = (NH + kYWarps - 1) / kYWarps;
+    const int ln = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    double re[KH], im[KH];
+    int2 sc[KH];
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int h = wq + kYWarps * k;
+      if (h < NH) {
+        re[k] = __ldg(Vt + h * 32 + ln);
+        im[k] = __ldg(Vt + (NH + h) * 32 + ln);
+        sc[k] = __ldg(reinterpret_cast<const int2*>(A.expand) + h);
+      }
     }
-    sX[(kXPad + f) * 32 + ln] = re;
-    sX[(NP + kXPad + f) * 32 + ln] = im;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int h = wq + kYWarps * k;
+      if (h < NH) {
+        sX[(kXPad + sc[k].x) * 32 + ln] = re[k];
+        sX[(NP + kXPad + sc[k].x) * 32 + ln] = im[k];
+        if (sc[k].y >= 0) {
+          const int fm = sc[k].y >> 1;
+          const bool neg = sc[k].y & 1;
+          sX[(kXPad + fm) * 32 + ln] = neg ? -re[k] : re[k];
+          sX[(NP + kXPad + fm) * 32 + ln] = neg ? im[k] : -im[k];
+        }
+      }
+    }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -855,8 +955,8 @@ __global__ void __launch_bounds__(384, 1) k_compute_Y_cwin(const YWArgs A) {
 #define YWROW(JJ)                                                                       \
   case JJ:                                                                              \
     if constexpr (JJ <= T) {                                                            \
-      if (2 * mb == JJ) yw_row<T, JJ, true>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc); \
-      else yw_row<T, JJ, false>(sX, sred, lane, w, nw, mb, rid, A, Yt, e_acc);          \
+      if (2 * mb == JJ) yw_row<T, JJ, true>(sX, sred, sW, lane, w, nw, mb, rid, A, Yt, e_acc); \
+      else yw_row<T, JJ, false>(sX, sred, sW, lane, w, nw, mb, rid, A, Yt, e_acc);          \
     }                                                                                   \
     break;
     switch (j) {
@@ -874,6 +974,8 @@ __global__ void __launch_bounds__(384, 1) k_compute_Y_cwin(const YWArgs A) {
     energy_epilogue(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
   }
 }
+
+#endif  // SNAP_T <= 8
 
 // ===========================================================================
 // compute_fused_dE  (snap_core.hpp:1274-1406): compute_dU fused with

@@ -57,6 +57,7 @@ static void launch_Y_window(snapgpu_ctx* c) {
 template <int T>
 void launch_Y_t(snapgpu_ctx* c) {
   constexpr int NH = c_half_off(T + 1);
+#if SNAP_T <= 8
   if constexpr (cw_base(T) >= 0) {
     if (c->y_impl == 0) {
       constexpr int NF = c_full_off(T + 1);
@@ -65,23 +66,23 @@ void launch_Y_t(snapgpu_ctx* c) {
       a.V = c->d_V.p;
       a.Y = c->d_Y.p;
       a.expand = c->d_expand.p;
-      a.items = c->d_witems.p;
       a.itw = c->d_citw.p;
-      a.rw_begin = c->d_rwbeg.p;
-      a.nwarps = c->ycplan.warps;
+      a.nitems = static_cast<int>(c->ycplan.items.size());
       a.tasks = c->d_tasks.p;
       a.task_cap = c->task_cap;
       a.nlocal = c->nlocal;
       a.E = energy_out(c);
-      const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)c->y_warps * (T + 1) * 2 * 32);
+      const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYWarps * (T + 1) * 2 * 32 +
+                                            (size_t)a.nitems);
       CK(cudaFuncSetAttribute(k_compute_Y_cwin<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem));
       dim3 grid(c->ntiles, c->y_parts_used);
-      k_compute_Y_cwin<T><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
+      k_compute_Y_cwin<T><<<grid, kYWarps * 32, smem, c->stream>>>(a);
       CK(cudaGetLastError());
       return;
     }
   }
+#endif
   constexpr int RED = 8 * (T + 1) * 2 * 32 * 8;
   if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
     if (c->y_ta == 32) return launch_Y_window<T, 32>(c);
@@ -122,26 +123,37 @@ void launch_DE_t(snapgpu_ctx* c) {
   }
 }
 
-// The windowed C' coefficients of the constant-window compute_Y live in this
-// object's constant bank (cCW, kernels.cuh), uploaded once per device.
+// The beta-independent tables of the constant-window compute_Y (windowed C',
+// packed row-pair items, [row][warp] ranges) live in this object's constant
+// bank (kernels.cuh), uploaded once per device.
 template <int T>
-void upload_cwin_t(int device, const YPlan& p) {
-  if constexpr (cw_base(T) >= 0) {
+void upload_ytables_t(int device, const YTablesHost& t) {
+#if SNAP_T <= 8
+  {
     static std::mutex mu;
     static std::vector<int> done;
     std::lock_guard<std::mutex> lk(mu);
     for (int d : done)
       if (d == device) return;
-    CK(cudaMemcpyToSymbol(cCW, p.cw.data(), p.cw.size() * sizeof(double),
-                          static_cast<size_t>(cw_base(T)) * sizeof(double)));
+    require(t.cw.size() == (size_t)c_cw_total(T), "compute_Y: C' table size mismatch");
+    require(t.items.size() <= (size_t)kYItemCap, "compute_Y: item table exceeds constant bank");
+    require(t.rw_begin.size() == (size_t)c_acc_off(T + 1) * (2 * kYWarps + 1),
+            "compute_Y: row/warp table size mismatch");
+    CK(cudaMemcpyToSymbol(cCW, t.cw.data(), t.cw.size() * sizeof(double)));
+    CK(cudaMemcpyToSymbol(cYItems, t.items.data(), t.items.size() * sizeof(uint4)));
+    CK(cudaMemcpyToSymbol(cYRowW, t.rw_begin.data(), t.rw_begin.size() * sizeof(int)));
     done.push_back(device);
   }
+#else
+  (void)device;
+  (void)t;
+#endif
 }
 
 template void launch_U_t<SNAP_T>(snapgpu_ctx*);
 template void launch_Y_t<SNAP_T>(snapgpu_ctx*);
 template void launch_DE_t<SNAP_T>(snapgpu_ctx*);
-template void upload_cwin_t<SNAP_T>(int, const YPlan&);
+template void upload_ytables_t<SNAP_T>(int, const YTablesHost&);
 
 }  // namespace host
 }  // namespace snapgpu

@@ -57,14 +57,14 @@ Fn pick_T(int T, Fn f0, Fn f1, Fn f2, Fn f3, Fn f4, Fn f5, Fn f6, Fn f7, Fn f8, 
                                  name<6>, name<7>, name<8>, name<9>, name<10>, name<11>, \
                                  name<12>, name<13>, name<14>)
 
-void upload_cwin(int device, int T, const YPlan& p) {
-  using Fn = void (*)(int, const YPlan&);
-  pick_T<Fn>(T, upload_cwin_t<0>, upload_cwin_t<1>, upload_cwin_t<2>, upload_cwin_t<3>,
-             upload_cwin_t<4>, upload_cwin_t<5>, upload_cwin_t<6>, upload_cwin_t<7>,
-             upload_cwin_t<8>, upload_cwin_t<9>, upload_cwin_t<10>, upload_cwin_t<11>,
-             upload_cwin_t<12>, upload_cwin_t<13>, upload_cwin_t<14>)(device, p);
+void upload_ytables(int device, int T, const YTablesHost& t) {
+  using Fn = void (*)(int, const YTablesHost&);
+  pick_T<Fn>(T, upload_ytables_t<0>, upload_ytables_t<1>, upload_ytables_t<2>,
+             upload_ytables_t<3>, upload_ytables_t<4>, upload_ytables_t<5>, upload_ytables_t<6>,
+             upload_ytables_t<7>, upload_ytables_t<8>, upload_ytables_t<9>, upload_ytables_t<10>,
+             upload_ytables_t<11>, upload_ytables_t<12>, upload_ytables_t<13>,
+             upload_ytables_t<14>)(device, t);
 }
-
 
 // compute_Y work split: TA atoms per CTA (32 when the V tile fits, smaller
 // tiles for small problems so the SMs fill), W warps per CTA owning target
@@ -75,7 +75,6 @@ void plan_y(snapgpu_ctx* c) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
   if (c->y_impl == 0) {  // one 32-atom tile per CTA, all warps per row
-    if (c->ycplan.warps != c->y_warps) build_ycoop(c);
     int parts = c->y_parts;
     // one CTA per SM: never exceed a single wave
     if (parts <= 0) parts = std::max(1, std::min(8, nsm / std::max(1, c->ntiles)));
@@ -115,29 +114,33 @@ void upload_beta(snapgpu_ctx* c) {
 }
 
 void build_ycoop(snapgpu_ctx* c) {
-  c->ycplan = ycoop_plan(c->maps, c->y_warps, true);
-  if (c->y_impl == 0) {  // constant-window items
-    std::vector<int> cwoff(c->maps.tuples.size());
-    int o = 0;
-    for (size_t q = 0; q < cwoff.size(); ++q) {
-      cwoff[q] = o;
-      o += (c->maps.tuples[q].j2 + 1) * (c->maps.tuples[q].j + 1);
-    }
-    std::vector<int4> wi(c->ycplan.items.size());
-    for (size_t q = 0; q < wi.size(); ++q) {
-      const Tuple& tp = c->maps.tuples[c->ycplan.items[q][0]];
-      const int D = (tp.j1 + tp.j2 - tp.j) / 2;
-      const int mb1 = c->ycplan.items[q][1], mb2 = c->ycplan.items[q][2];
-      wi[q] = make_int4(c->maps.full_off[tp.j1] + mb1 * (tp.j1 + 1) + D,
-                        c->maps.full_off[tp.j2] + mb2 * (tp.j2 + 1),
-                        tp.j2 | (cwoff[c->ycplan.items[q][0]] << 8), 0);
-    }
-    c->d_witems.alloc(std::max<size_t>(1, wi.size()));
-    CK(cudaMemcpy(c->d_witems.p, wi.data(), wi.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  c->ycplan = ycoop_pair_plan(c->maps, kYWarps);
+  // constant-window units, packed for the constant bank (kernels.cuh cYItems)
+  std::vector<int> cwoff(c->maps.tuples.size());
+  int o = 0;
+  for (size_t q = 0; q < cwoff.size(); ++q) {
+    cwoff[q] = o;
+    o += (c->maps.tuples[q].j2 + 1) * (c->maps.tuples[q].j + 1);
   }
-  c->d_rwbeg.alloc(c->ycplan.rw_begin.size());
-  CK(cudaMemcpy(c->d_rwbeg.p, c->ycplan.rw_begin.data(), c->ycplan.rw_begin.size() * sizeof(int),
-                cudaMemcpyHostToDevice));
+  auto rows = [&](int i) {  // x1 window base | x2 row base << 16 of item i
+    const Tuple& tp = c->maps.tuples[c->ycplan.items[i][0]];
+    const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+    const int mb1 = c->ycplan.items[i][1], mb2 = c->ycplan.items[i][2];
+    const unsigned x1 = c->maps.full_off[tp.j1] + mb1 * (tp.j1 + 1) + D;
+    const unsigned x2 = c->maps.full_off[tp.j2] + mb2 * (tp.j2 + 1);
+    return x1 | (x2 << 16);
+  };
+  YTablesHost t;
+  t.cw = c->yplan.cw;
+  t.rw_begin = c->ycplan.rw_begin;
+  t.items.resize(c->ycplan.units.size());
+  for (size_t u = 0; u < t.items.size(); ++u) {
+    const int i0 = c->ycplan.units[u][0], n = c->ycplan.units[u][1];
+    const Tuple& tp = c->maps.tuples[c->ycplan.items[i0][0]];
+    t.items[u] = make_uint4(rows(i0), tp.j2 | (cwoff[c->ycplan.items[i0][0]] << 8),
+                            rows(n == 2 ? i0 + 1 : i0), static_cast<unsigned>(i0));
+  }
+  upload_ytables(c->device, c->T, t);
   upload_beta(c);
 }
 
@@ -392,9 +395,8 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
       if (std::string(e) == "window") c->y_impl = 2;
     if (c->y_impl == 0) {
       c->y_warps = 12;
-      up(c->d_expand, full_expand_map(c->maps));
-      upload_cwin(device, twojmax, c->yplan);
-      build_ycoop(c);  // uploads the beta-dependent item weights
+      up(c->d_expand, half_scatter_map(c->maps));
+      build_ycoop(c);  // constant-bank tables + the beta-dependent item weights
     } else {
       upload_beta(c);
     }
@@ -426,8 +428,6 @@ int snapgpu_destroy(snapgpu_ctx* c) {
 
   c->d_citw.release();
   c->d_expand.release();
-  c->d_rwbeg.release();
-  c->d_witems.release();
   c->d_tasks.release();
   c->d_numneigh.release();
   c->d_nbr.release();
@@ -781,8 +781,8 @@ int snapgpu_stage_times(snapgpu_ctx* c, float* out4) {
 int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int y_tile_atoms) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    require(y_warps >= 0 && y_warps <= (c->y_impl == 0 ? 12 : 8),
-            "tune: y_warps in [0,12] (2J <= 8) or [0,8]");
+    require(c->y_impl == 0 ? (y_warps == 0 || y_warps == kYWarps) : (y_warps >= 0 && y_warps <= 8),
+            "tune: y_warps must be 12 (2J <= 8) or in [0,8]");
     require(y_tile_atoms == 0 || y_tile_atoms == 8 || y_tile_atoms == 16 || y_tile_atoms == 32,
             "tune: y_tile_atoms in {0, 8, 16, 32}");
     if (y_warps > 0) c->y_warps = y_warps;

@@ -183,20 +183,21 @@ std::vector<double> half_ywgt(const IndexMaps& m) {
   return out;
 }
 
-std::vector<int> full_expand_map(const IndexMaps& m) {
-  std::vector<int> out(m.nfull);
+// Scatter map of the half stack into the full mirrored stack (compute_Y
+// X tile): out[2h] = full index of half element h = (t, mb, ma); out[2h+1] =
+// full index fm of its mirror (t, t-mb, t-ma) times 2 plus the sign bit
+// (u(t-mb,t-ma) = (-1)^(ma+mb) conj u(mb,ma), halfint_index.hpp:22-25), or -1
+// on a middle row, which the half storage holds completely.
+std::vector<int> half_scatter_map(const IndexMaps& m) {
+  std::vector<int> out(2 * m.nhalf);
   for (int t = 0; t <= m.T; ++t)
-    for (int mb = 0; mb <= t; ++mb)
+    for (int mb = 0; 2 * mb <= t; ++mb)
       for (int ma = 0; ma <= t; ++ma) {
-        int code;
-        if (2 * mb <= t) {
-          code = (m.half_off[t] + mb * (t + 1) + ma) * 4;
-        } else {
-          const int src = m.half_off[t] + (t - mb) * (t + 1) + (t - ma);
-          const bool neg = ((ma + mb) & 1) != 0;
-          code = src * 4 + 2 + (neg ? 1 : 0);
-        }
-        out[m.full_off[t] + mb * (t + 1) + ma] = code;
+        const int h = m.half_off[t] + mb * (t + 1) + ma;
+        out[2 * h] = m.full_off[t] + mb * (t + 1) + ma;
+        out[2 * h + 1] = (2 * mb < t)
+                             ? 2 * (m.full_off[t] + (t - mb) * (t + 1) + (t - ma)) + ((ma + mb) & 1)
+                             : -1;
       }
   return out;
 }
@@ -320,6 +321,55 @@ YCoopPlan ycoop_plan(const IndexMaps& m, int warps, bool lpt_split) {
         p.rw_begin.push_back(off);
         for (int idx : buckets[w]) p.items.push_back(its[idx]);
         off = static_cast<int>(p.items.size());
+      }
+      p.rw_begin.push_back(off);
+    }
+  return p;
+}
+
+YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps) {
+  YCoopPlan p;
+  p.warps = warps;
+  for (int j = 0; j <= m.T; ++j)
+    for (int mb = 0; 2 * mb <= j; ++mb) {
+      const int nout = (2 * mb == j) ? j / 2 + 1 : j + 1;
+      // units of this row: consecutive mb1 of one tuple paired up
+      std::vector<std::vector<std::array<int, 4>>> units;
+      std::vector<std::pair<double, int>> costs;
+      double tot = 0.0;
+      int local = -1;
+      for (std::size_t q = 0; q < m.tuples.size(); ++q) {
+        const Tuple& tp = m.tuples[q];
+        if (tp.j != j) continue;
+        ++local;
+        const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+        const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
+        for (int mb1 = lo; mb1 <= hi; mb1 += 2) {
+          std::vector<std::array<int, 4>> u;
+          u.push_back({static_cast<int>(q), mb1, mb + D - mb1, local});
+          if (mb1 + 1 <= hi) u.push_back({static_cast<int>(q), mb1 + 1, mb + D - mb1 - 1, local});
+          // FP64 instructions: 6 per MAC single, 10 per pair MAC; plus setup
+          const double c = (tp.j2 + 1) * ((u.size() == 2 ? 10.0 : 6.0) * nout + 8.0) +
+                           (u.size() == 2 ? 60.0 : 40.0);
+          costs.push_back({c, static_cast<int>(units.size())});
+          units.push_back(u);
+          tot += c;
+        }
+      }
+      p.row_cost.push_back(tot);
+      std::vector<std::vector<int>> buckets = lpt(costs, warps);
+      int off = static_cast<int>(p.units.size());
+      for (int w = 0; w < warps; ++w) {
+        std::sort(buckets[w].begin(), buckets[w].end());
+        for (int kind = 2; kind >= 1; --kind) {  // pairs, then singles
+          p.rw_begin.push_back(off);
+          for (int idx : buckets[w]) {
+            if (static_cast<int>(units[idx].size()) != kind) continue;
+            p.units.push_back({static_cast<int>(p.items.size()), kind});
+            for (const auto& it : units[idx]) p.items.push_back(it);
+          }
+          off = static_cast<int>(p.units.size());
+        }
       }
       p.rw_begin.push_back(off);
     }

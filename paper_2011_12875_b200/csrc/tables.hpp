@@ -69,7 +69,7 @@ std::vector<double> half_ywgt(const IndexMaps& m);
 // Full-index expansion map for the Y kernel: for full index (t,mb,ma),
 // src half index and sign (+1, or -1 with conj when mirrored).  Encoded
 // as src*4 + (mirrored?2:0) + (negative?1:0).
-std::vector<int> full_expand_map(const IndexMaps& m);
+std::vector<int> half_scatter_map(const IndexMaps& m);
 
 
 // compute_Y row-pair items (sliding-window kernel, kernels.cuh k_compute_Y).
@@ -95,8 +95,14 @@ struct YCoopPlan {
   std::vector<std::array<int, 4>> items;
   std::vector<int> rw_begin;
   std::vector<double> row_cost;
+  // paired plan only: units {first item, item count 1|2}; the two items of a
+  // pair share (tuple, target row), so they share every C' coefficient.
+  // rw_begin then holds 2*warps+1 bounds per row: [pairs of warp 0, singles
+  // of warp 0, pairs of warp 1, ...].
+  std::vector<std::array<int, 2>> units;
 };
 YCoopPlan ycoop_plan(const IndexMaps& m, int warps, bool lpt_split);
+YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps);
 std::vector<double> ycoop_weights(const YCoopPlan& p, const IndexMaps& m,
                                   const std::vector<double>& wtab);
 // LPT assignment of rows to workers: [worker][cap] row codes j*64+mb, -1 end.

@@ -221,7 +221,7 @@ def test_stage_timing_and_tuning_knobs(snap):
     base = snap.run_pipeline(p)
     eng = snap.SnapEngine.for_problem(p)
     eng.set_problem(p)
-    for yw, yp, ta in [(4, 1, 0), (8, 2, 32), (6, 3, 16), (8, 1, 8), (2, 0, 0)]:
+    for yw, yp, ta in [(0, 1, 0), (12, 2, 32), (0, 3, 16), (0, 1, 8), (0, 0, 0), (0, 7, 0)]:
         eng.tune(y_warps=yw, y_parts=yp, y_tile_atoms=ta)
         eng.enable_stage_timing(True)
         eng.run()
