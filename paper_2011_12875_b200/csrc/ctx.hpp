@@ -90,6 +90,7 @@ struct snapgpu_ctx {
   snapgpu::YCoopPlan ycplan;
   int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
   int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
+  int u_impl = 0;   // 0: row-lane compute_U (2J <= 8), 1: column-lane compute_U
   int task_cap = 0;
   int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
   int y_ta = 32, y_ta_max = 32, y_ta_req = 0;

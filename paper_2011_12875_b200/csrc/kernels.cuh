@@ -405,6 +405,229 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32, SNAP_U_MINB)
   }
 }
 
+// ===========================================================================
+// compute_U, row-lane variant (2J <= 8)
+//
+// Lanes = (atom a, pair slot s, row r): a warp accumulates APW atoms at once,
+// each with SL pair slots (2 for large problems, 8 when the atoms are too few
+// to fill the SMs) of G row lanes (G = rows of the half level,
+// the fused-dE layout).  Lane r owns row mb = r of the current level (T+1
+// complex in registers) and advances it in place, v(t,r,c) = conj(a)
+// v(t-1,r,c) - conj(b) v(t-1,r,c-1): no shuffles except the seeding of a new
+// middle row from the mirror of the row above (one shfl_up per column); the
+// last middle row (even 2J) is produced transiently by lane T/2-1 for
+// c <= T/2 and mirrored at the write.  The neighbor sum of the lane's row at
+// every level stays in registers (acc[t(t+1)/2 + c]) across the passes over
+// the atom's pairs; one xor-shuffle then combines the two slots and the
+// atom's V row is written once.  All lanes do useful recursion work on their
+// own row (no idle columns), the geometry of every pair is computed once
+// into shared memory by a prepass that also restates Problem::validate.
+// ===========================================================================
+#ifndef SNAP_U2_MINB
+#define SNAP_U2_MINB 1
+#endif
+template <int T, int SL_ = 2>
+struct U2Cfg {
+  static constexpr int NL = (T == 0) ? 1 : ((T & 1) == 0 ? T / 2 : (T + 1) / 2);
+  static constexpr int G = NL <= 1 ? 1 : NL <= 2 ? 2 : NL <= 4 ? 4 : NL <= 8 ? 8 : 16;
+  static constexpr int SL = SL_ * G <= 32 ? SL_ : 32 / G;  // pair slots per atom
+  static constexpr int APW = 32 / (G * SL);    // atoms per warp
+  static constexpr int NC = T + 1;
+  static constexpr int NACC = (T + 1) * (T + 2) / 2;  // (t, c) of one row, all levels
+  static constexpr int NH = c_half_off(T + 1);
+  static constexpr int WARPS = 4;
+};
+
+template <int T, int SL>
+__global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
+    k_compute_U2(const UArgs A) {
+  using C = U2Cfg<T, SL>;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int S = A.pr.stride;
+  const int i0 = (blockIdx.x * C::WARPS + w) * C::APW;  // first atom of the warp
+  if (A.pr.types) {  // type range of every atom (grid-strided)
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < A.pr.natoms_total;
+         a += gridDim.x * blockDim.x) {
+      const int ty = A.pr.types[a];
+      if (ty < 0 || ty >= A.pr.nweights) atomicOr(A.pr.err, kErrType);
+    }
+  }
+  if (i0 >= A.pr.nlocal) return;  // whole warp
+  double* geo = smem + (size_t)w * C::APW * S * 5;  // [atom][pair][ar ai br bi sfac]
+
+  // ---- prepass: validation + geometry of the warp's pairs ----
+  for (int idx = lane; idx < C::APW * S; idx += 32) {
+    const int a = idx / S, k = idx - a * S;
+    const int i = i0 + a;
+    if (i >= A.pr.nlocal) continue;
+    int nn = A.pr.numneigh[i];
+    if (nn < 0 || nn > S) {
+      if (k == 0) atomicOr(A.pr.err, kErrCount);
+      continue;
+    }
+    if (k >= nn) continue;
+    const size_t pk = (size_t)i * S + k;
+    const double* d = A.pr.disp + pk * 3;
+    const int j = A.pr.nbr[pk];
+    const double rsq = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+    unsigned bad = 0u;
+    if (j < 0 || j >= A.pr.natoms_total) bad |= kErrIndex;
+    if (j == A.pr.atom_lo + i) bad |= kErrSelf;
+    if (!(rsq > 0.0)) bad |= kErrZero;
+    if (!(rsq < A.pr.rc2)) bad |= kErrCut;
+    double wj = 0.0;
+    if (!(bad & kErrIndex)) {
+      const int ty = A.pr.types ? A.pr.types[j] : 0;
+      if (ty >= 0 && ty < A.pr.nweights) wj = A.pr.weights[ty];
+    }
+    if (bad) atomicOr(A.pr.err, bad);
+    PairGeo g;
+    pair_geometry<false>(d[0], d[1], d[2], wj, A.gp, g);
+    double* o = geo + (size_t)idx * 5;
+    o[0] = g.ar;
+    o[1] = g.ai;
+    o[2] = g.br;
+    o[3] = g.bi;
+    o[4] = g.sfac;
+  }
+  __syncwarp();
+
+  const int r = lane % C::G;
+  const int s = (lane / C::G) % C::SL;
+  const int a = lane / (C::G * C::SL);
+  const int i = i0 + a;
+  int nn = 0;
+  if (i < A.pr.nlocal) {
+    nn = A.pr.numneigh[i];
+    if (nn < 0 || nn > S) nn = 0;
+  }
+  int passes = (nn + C::SL - 1) / C::SL;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) passes = max(passes, __shfl_xor_sync(0xffffffffu, passes, o));
+
+  double accr[C::NACC], acci[C::NACC];
+#pragma unroll
+  for (int q = 0; q < C::NACC; ++q) accr[q] = acci[q] = 0.0;
+  constexpr int NM = (T & 1) == 0 ? T / 2 + 1 : 1;  // transient last middle row
+  double amr[NM], ami[NM];
+#pragma unroll
+  for (int q = 0; q < NM; ++q) amr[q] = ami[q] = 0.0;
+
+  for (int p = 0; p < passes; ++p) {
+    const int k = p * C::SL + s;
+    double ar = 1.0, ai = 0.0, br = 0.0, bi = 0.0, sf = 0.0;
+    if (k < nn) {
+      const double* g = geo + (size_t)(a * S + k) * 5;
+      ar = g[0];
+      ai = g[1];
+      br = g[2];
+      bi = g[3];
+      sf = g[4];
+    }
+    double vr[C::NC], vi[C::NC];
+#pragma unroll
+    for (int c = 0; c < C::NC; ++c) vr[c] = vi[c] = 0.0;
+    vr[0] = (r == 0) ? 1.0 : 0.0;
+    accr[0] += sf * vr[0];
+#pragma unroll
+    for (int t = 1; t <= T; ++t) {
+      if ((t & 1) == 0 && t < T + (T & 1)) {  // seed the new middle row t/2
+        const bool creator = (2 * r == t);
+        const double R = mirror_R(t);
+#pragma unroll
+        for (int c = 0; c < t; ++c) {
+          const double K = (((c + t / 2) & 1) ? -R : R);
+          const double sr = __shfl_up_sync(0xffffffffu, vr[t - 1 - c], 1);
+          const double si = __shfl_up_sync(0xffffffffu, vi[t - 1 - c], 1);
+          if (creator) {
+            vr[c] = K * sr;
+            vi[c] = -K * si;
+          }
+        }
+      }
+      if (t == T && (T & 1) == 0 && 2 * r + 2 == T) {  // transient last middle row
+        const double R = mirror_R(T);
+        double plr = 0.0, pli = 0.0;
+#pragma unroll
+        for (int c = 0; c <= T / 2; ++c) {
+          const double K = (((c + T / 2) & 1) ? -R : R);
+          const double pr = K * vr[T - 1 - c], pi = -K * vi[T - 1 - c];
+          const double nr = ar * pr + ai * pi - br * plr - bi * pli;
+          const double ni = ar * pi - ai * pr - br * pli + bi * plr;
+          amr[c] = fma(sf, nr, amr[c]);
+          ami[c] = fma(sf, ni, ami[c]);
+          plr = pr;
+          pli = pi;
+        }
+      }
+      // every lane advances its row (rows that do not exist yet are zero
+      // and stay zero: no divergent branch)
+#pragma unroll
+      for (int c = t; c >= 0; --c) {
+        const double pr = (c < t) ? vr[c] : 0.0, pi = (c < t) ? vi[c] : 0.0;
+        const double qr = (c > 0) ? vr[c - 1] : 0.0, qi = (c > 0) ? vi[c - 1] : 0.0;
+        const double nr = ar * pr + ai * pi - br * qr - bi * qi;
+        const double ni = ar * pi - ai * pr - br * qi + bi * qr;
+        vr[c] = nr;
+        vi[c] = ni;
+        accr[t * (t + 1) / 2 + c] = fma(sf, nr, accr[t * (t + 1) / 2 + c]);
+        acci[t * (t + 1) / 2 + c] = fma(sf, ni, acci[t * (t + 1) / 2 + c]);
+      }
+    }
+  }
+  // combine the pair slots of each atom
+#pragma unroll
+  for (int o = C::G; o < C::G * C::SL; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < C::NACC; ++q) {
+      accr[q] += __shfl_xor_sync(0xffffffffu, accr[q], o);
+      acci[q] += __shfl_xor_sync(0xffffffffu, acci[q], o);
+    }
+#pragma unroll
+    for (int q = 0; q < NM; ++q) {
+      amr[q] += __shfl_xor_sync(0xffffffffu, amr[q], o);
+      ami[q] += __shfl_xor_sync(0xffffffffu, ami[q], o);
+    }
+  }
+  if (s != 0 || r >= C::NL || i >= A.pr.nlocal) return;
+  const double inv_sqrt_fact[8] = {1.0, 1.0, 0.70710678118654752440, 0.40824829046386301637,
+                                   0.20412414523193150819, 0.091287092917527685576,
+                                   0.037267799624996494940, 0.014085904245475275327};
+  const double self = A.gp.self_flag ? A.gp.wself : 0.0;
+  double* Vr = A.V + ((size_t)(i >> 5) * 2 * C::NH) * 32 + (i & 31);
+  double* Vi = Vr + (size_t)C::NH * 32;
+#pragma unroll
+  for (int t = 0; t <= T; ++t) {
+    if (2 * r > t) continue;
+#pragma unroll
+    for (int c = 0; c <= t; ++c) {
+      double vr_ = accr[t * (t + 1) / 2 + c];
+      if (c == r) vr_ += self * inv_sqrt_fact[r];  // wself * f(t,mb,mb) (snap_core.hpp:404-413)
+      const int h = c_half_off(t) + r * (t + 1) + c;
+      Vr[(size_t)h * 32] = vr_;
+      Vi[(size_t)h * 32] = acci[t * (t + 1) / 2 + c];
+    }
+  }
+  if ((T & 1) == 0 && T > 0 && 2 * r + 2 == T) {
+    // last middle row (T, T/2): c <= T/2 computed, the rest by the mirror
+    // v(T/2, T-c) = (-1)^(c+T/2) conj v(T/2, c)
+    const int hb = c_half_off(T) + (T / 2) * (T + 1);
+#pragma unroll
+    for (int c = 0; c <= T / 2; ++c) {
+      double mr = amr[c];
+      if (c == T / 2) mr += self * inv_sqrt_fact[T / 2];
+      Vr[(size_t)(hb + c) * 32] = mr;
+      Vi[(size_t)(hb + c) * 32] = ami[c];
+      if (c < T / 2) {
+        const double sg = ((c + T / 2) & 1) ? -1.0 : 1.0;
+        Vr[(size_t)(hb + T - c) * 32] = sg * mr;
+        Vi[(size_t)(hb + T - c) * 32] = -sg * ami[c];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Energy epilogue shared by the compute_Y kernels: per-atom energies are
 // accumulated into eatom (atomics; one add per CTA that touched the atom), the
@@ -1249,11 +1472,13 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
   const double ar = g.ar, ai = g.ai, br = g.br, bi = g.bi;
 
   // ---------------- forward ----------------
+  // v level by level; only the level inputs are saved (the contraction
+  // value F comes out of the backward sweep, see below), so this sweep
+  // reads no Y' at all.
   double vr[C::NC], vi[C::NC];
 #pragma unroll
   for (int c = 0; c < C::NC; ++c) vr[c] = vi[c] = 0.0;
   vr[0] = (r == 0) ? 1.0 : 0.0;
-  double F = (r == 0) ? __ldg(Y2).x : 0.0;
 #pragma unroll
   for (int t = 1; t <= T; ++t) {
     if ((t & 1) == 0 && t < T + (T & 1)) {  // seed the new middle row t/2
@@ -1278,38 +1503,13 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
         buf[(size_t)(2 * (o + c)) * 32] = vr[c];
         buf[(size_t)(2 * (o + c) + 1) * 32] = vi[c];
       }
-    }
-    if (t == T && (T & 1) == 0 && 2 * r + 2 == T) {  // transient last middle row
-      const double R = mirror_R(T);
-      const int hb = c_half_off(T) + (T / 2) * (T + 1);
-      double plr = 0.0, pli = 0.0;
+      if (t < T) {  // the level-T row is never an input
 #pragma unroll
-      for (int c = 0; c <= T / 2; ++c) {
-        const double K = (((c + T / 2) & 1) ? -R : R);
-        const double pr = K * vr[T - 1 - c], pi = -K * vi[T - 1 - c];
-        const double nr = ar * pr + ai * pi - br * plr - bi * pli;
-        const double ni = ar * pi - ai * pr - br * pli + bi * plr;
-        {
-          const double2 yv = __ldg(Y2 + hb + c);
-          F += nr * yv.x + ni * yv.y;
-        }
-        plr = pr;
-        pli = pi;
-      }
-    }
-    if (active) {
-      const int hb = c_half_off(t) + r * (t + 1);
-#pragma unroll
-      for (int c = t; c >= 0; --c) {
-        const double pr = (c < t) ? vr[c] : 0.0, pi = (c < t) ? vi[c] : 0.0;
-        const double qr = (c > 0) ? vr[c - 1] : 0.0, qi = (c > 0) ? vi[c - 1] : 0.0;
-        const double nr = ar * pr + ai * pi - br * qr - bi * qi;
-        const double ni = ar * pi - ai * pr - br * qi + bi * qr;
-        vr[c] = nr;
-        vi[c] = ni;
-        {
-          const double2 yv = __ldg(Y2 + hb + c);
-          F += nr * yv.x + ni * yv.y;
+        for (int c = t; c >= 0; --c) {
+          const double pr = (c < t) ? vr[c] : 0.0, pi = (c < t) ? vi[c] : 0.0;
+          const double qr = (c > 0) ? vr[c - 1] : 0.0, qi = (c > 0) ? vi[c - 1] : 0.0;
+          vr[c] = ar * pr + ai * pi - br * qr - bi * qi;
+          vi[c] = ar * pi - ai * pr - br * qi + bi * qr;
         }
       }
     }
@@ -1317,6 +1517,10 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
   __syncwarp();
 
   // ---------------- backward ----------------
+  // F = Re sum_t <Y'_t, v_t> telescopes through the adjoints: with
+  // lambda_t = Y'_t + A_{t+1}^H lambda_{t+1} (A_t the R-linear level map),
+  // F = Re <lambda_0, v_0> = Re lambda_0(0,0) since v_0 = 1.
+  double F = (T == 0 && r == 0) ? __ldg(Y2).x : 0.0;  // 2J = 0: no levels to sweep
   double Gar = 0.0, Gai = 0.0, Gbr = 0.0, Gbi = 0.0;
   double lr[C::NC], li[C::NC];  // lambda_t(r, c)
 #pragma unroll
@@ -1397,6 +1601,7 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
         gi_[t - 1 - c] += recv ? si_[c] : 0.0;
       }
     }
+    if (t == 1 && r == 0) F = __ldg(Y2).x + gr_[0];  // Re lambda_0(0,0)
     // lambda_{t-1} for rows that already existed at level t-1
     if (t > 1) {
       const bool keep = 2 * r <= t - 1;

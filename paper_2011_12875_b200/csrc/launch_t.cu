@@ -12,8 +12,33 @@
 namespace snapgpu {
 namespace host {
 
+template <int T, int SL>
+static void launch_U2(snapgpu_ctx* c) {
+  using C2 = U2Cfg<T, SL>;
+  UArgs a;
+  a.pr = pair_args(c);
+  a.gp = c->gp;
+  a.V = c->d_V.p;
+  const size_t smem = sizeof(double) * (size_t)C2::WARPS * C2::APW * c->stride * 5;
+  CK(cudaFuncSetAttribute(k_compute_U2<T, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::max<size_t>(smem, 48 * 1024)));
+  const int per_block = C2::WARPS * C2::APW;
+  const int blocks = (c->nlocal + per_block - 1) / per_block;
+  k_compute_U2<T, SL><<<blocks, C2::WARPS * 32, smem, c->stream>>>(a);
+  CK(cudaGetLastError());
+}
+
 template <int T>
 void launch_U_t(snapgpu_ctx* c) {
+  if constexpr (T <= 8) {
+    if (c->u_impl == 0) {  // row-lane kernel
+      // two pair slots per atom when the atoms fill the SMs, else eight
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+      if (c->nlocal / U2Cfg<T, 2>::APW >= 8 * nsm) return launch_U2<T, 2>(c);
+      return launch_U2<T, 8>(c);
+    }
+  }
   using C = UCfg<T>;
   UArgs a;
   a.pr = pair_args(c);

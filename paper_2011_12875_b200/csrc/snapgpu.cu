@@ -391,6 +391,9 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     c->de_impl = (twojmax <= 10) ? 0 : 1;  // reverse mode needs ~8 register rows
     if (const char* e = std::getenv("SNAPGPU_DE_IMPL"))  // A/B switch for development
       c->de_impl = (std::string(e) == "forward") ? 1 : 0;
+    c->u_impl = (twojmax <= 8) ? 0 : 1;
+    if (const char* e = std::getenv("SNAPGPU_U_IMPL"))  // A/B switch for development
+      if (std::string(e) == "column") c->u_impl = 1;
     if (const char* e = std::getenv("SNAPGPU_Y_IMPL"))  // A/B switch for development
       if (std::string(e) == "window") c->y_impl = 2;
     if (c->y_impl == 0) {

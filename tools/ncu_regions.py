@@ -10,8 +10,14 @@ dominant stall reasons (development helper).
 import csv, re, sys
 from collections import Counter, defaultdict
 
-rows = list(csv.reader(open(sys.argv[1])))
+allrows = list(csv.reader(open(sys.argv[1])))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 15
+want = sys.argv[3] if len(sys.argv) > 3 else None  # kernel-name substring
+starts = [i for i, r in enumerate(allrows) if r and r[0] == 'Kernel Name']
+sec = [(i, j) for i, j in zip(starts, starts[1:] + [len(allrows)])
+       if want is None or want in allrows[i][1]][0]
+rows = allrows[sec[0]:sec[1]]
+print(rows[0][1])
 h = rows[1]
 ix = {k: i for i, k in enumerate(h)}
 stall_cols = [k for k in h if k.startswith('stall_') and '(Not Issued)' not in k]
