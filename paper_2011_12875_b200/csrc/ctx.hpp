@@ -83,17 +83,18 @@ struct snapgpu_ctx {
   std::vector<double> cg, hf, ywgt;
 
   // device tables
-  snapgpu::host::DevBuf<double> d_weights, d_itw, d_cw, d_citw;
+  snapgpu::host::DevBuf<double> d_weights, d_itw, d_cw, d_citw[2];
   snapgpu::host::DevBuf<int4> d_items;
   snapgpu::host::DevBuf<int> d_rowbeg, d_tasks, d_expand;
   snapgpu::YPlan yplan;
-  snapgpu::YCoopPlan ycplan;
+  snapgpu::YCoopPlan ycplan[2];  // constant-window units for 4 / 12 warps per row
   int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
   int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
   int u_impl = 0;   // 0: row-lane compute_U (2J <= 8), 1: column-lane compute_U
   int task_cap = 0;
   int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
   int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
+  int y_groups = 3;  // warp groups per constant-window compute_Y CTA (1 or 3)
 
   // problem shape
   int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
@@ -155,10 +156,13 @@ template <int T> void launch_Y_t(snapgpu_ctx* c);
 template <int T> void launch_DE_t(snapgpu_ctx* c);
 struct YTablesHost {  // constant-bank tables of k_compute_Y_cwin (kernels.cuh)
   std::vector<double> cw;
-  std::vector<uint4> items;
-  std::vector<int> rw_begin;
+  std::vector<uint4> items4, items12;
+  std::vector<int> rw4, rw12;
 };
 template <int T> void upload_ytables_t(int device, const YTablesHost& t);
+#ifdef SNAP_Y_PROFILE
+extern long long* g_yprof;  // per-row cycle sums of k_compute_Y_cwin (calibration builds)
+#endif
 
 }  // namespace host
 }  // namespace snapgpu

@@ -917,8 +917,27 @@ __host__ __device__ constexpr int cw_base(int T) {  // windowed C' of 2J = 0..8 
 // X planes carry kXPad zero elements on each side: the window reads reach
 // kXPad >= J2 + 1 = 9 below the first row and D <= 8 above the last.
 constexpr int kXPad = 12;
-constexpr int kYWarps = 12;      // warps per k_compute_Y_cwin CTA
-constexpr int kYItemCap = 1536;  // row-pair units at 2J = 8: 838 (1479 items)
+#ifndef SNAP_Y_WARPS
+#define SNAP_Y_WARPS 12
+#endif
+constexpr int kYWarps = SNAP_Y_WARPS;  // warps per k_compute_Y_cwin CTA
+// A CTA runs as GR independent groups of kYWarps/GR warps: GR = 3 (large
+// problems: a group owns whole target rows, with its own row list, named
+// barrier and slice of the partial-row buffer, so rows synchronise 4 warps
+// only and the groups drift independently) or GR = 1 (small problems split
+// over several CTAs per tile: all 12 warps on one row at a time, the finest
+// row granularity).  The row-pair units of every target row are LPT-split
+// over the group's warps; each layout has its own unit table, sorted by
+// tuple within a warp so the warps of a group sweep the C' table together.
+template <int GR>
+__device__ __forceinline__ void group_sync(int g) {
+  if constexpr (GR == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"((kYWarps / GR) * 32) : "memory");
+  }
+}
+constexpr int kYItemCap = 1024;  // row-pair units at 2J = 8: 838 (1479 items)
 #ifndef SNAP_Y_PAIR_U
 #define SNAP_Y_PAIR_U 2
 #endif
@@ -927,15 +946,18 @@ constexpr int kYPairU = SNAP_Y_PAIR_U;  // window block length of the paired loo
 // beta-independent tables of the constant-window kernel, in the constant bank
 // of the per-2J object (launch_t.cu, uploaded once per device): warp-uniform
 // reads, so every access is a broadcast from the constant cache.
-//   cCW     windowed C' coefficients, rows of length j+1 per (tuple, a2)
-//   cYItems row-pair units {x1 window base (full idx + D) | x2 row base << 16,
-//           J2 | C' offset << 8, same x1|x2 of the second item, W index},
-//           grouped by target row, then by warp (pairs, then singles)
-//   cYRowW  [row][2*warp+kind] unit ranges
+//   cCW       windowed C' coefficients, rows of length j+1 per (tuple, a2)
+//   cYItemsG  row-pair units {x1 window base (full idx + D) | x2 row base << 16,
+//             J2 | C' offset << 8, same x1|x2 of the second item, W index},
+//             grouped by target row, then by warp (pairs, then singles), for
+//             G = 4 or 12 warps per row
+//   cYRowWG   [row][2*warp+kind] unit ranges
 #if defined(SNAP_T) && SNAP_T <= 8
 __constant__ double cCW[c_cw_total(SNAP_T)];
-__constant__ uint4 cYItems[kYItemCap];
-__constant__ int cYRowW[c_acc_off(SNAP_T + 1) * (2 * kYWarps + 1)];
+__constant__ uint4 cYItems4[kYItemCap];
+__constant__ uint4 cYItems12[kYItemCap];
+__constant__ int cYRowW4[c_acc_off(SNAP_T + 1) * (2 * 4 + 1)];
+__constant__ int cYRowW12[c_acc_off(SNAP_T + 1) * (2 * 12 + 1)];
 #endif
 
 struct YWArgs {
@@ -944,6 +966,7 @@ struct YWArgs {
   const int* expand;    // half -> full scatter map (tables.cpp:half_scatter_map)
   const double* itw;    // W per item (beta-dependent; staged into shared memory)
   int nitems;
+  long long* prof;      // SNAP_Y_PROFILE builds: per-row cycle sums (else unused)
   const int* tasks;
   int task_cap;
   int nlocal;
@@ -960,12 +983,12 @@ struct YWArgs {
 // below hold the elements entering during a block of U steps, so step u of a
 // block reads E[U-1+ma-u] (compile-time index) and only one re-alignment per
 // block is needed.
-template <int G, int U, int L, int JW, int NP>
+template <int G, int U, int L, int JW, int NP, int GW>
 __device__ __forceinline__ void yw_units(const double* __restrict__ sX,
                                          const double* __restrict__ sW, int lane, int b, int e,
                                          double (&ar)[L], double (&ai)[L]) {
   for (int it = b; it < e; ++it) {
-    const uint4 m = cYItems[it];
+    const uint4 m = (GW == 4) ? cYItems4[it] : cYItems12[it];
     const int J2 = m.y & 0xff;
     const double* c0 = cCW + (m.y >> 8);
     const double* p1[G];
@@ -1073,28 +1096,31 @@ __device__ __forceinline__ void yw_units(const double* __restrict__ sX,
   }
 }
 
-template <int T, int J, bool MID>
+template <int T, int J, bool MID, int GR>
 __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __restrict__ sred,
                                        const double* __restrict__ sW,
-                                       int lane, int w, int nw, int mb, int rid, const YWArgs& A,
+                                       int lane, int g, int w, int mb, int rid, const YWArgs& A,
                                        double* __restrict__ Yt, double& e_acc) {
+  // g = group, w = warp within the group; sred = the group's slice
   constexpr int NF = c_full_off(T + 1);
   constexpr int NP = NF + 2 * kXPad;  // padded plane length
   constexpr int NH = c_half_off(T + 1);
   constexpr int L = MID ? J / 2 + 1 : J + 1;
   constexpr int JW = J + 1;
+  constexpr int nw = kYWarps / GR;
+  static_assert(nw == 4 || nw == 12, "unit tables exist for 4 and 12 warps per row");
   double ar[L], ai[L];
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
-  const int* rb = cYRowW + rid * (2 * kYWarps + 1) + 2 * w;
-  yw_units<2, kYPairU, L, JW, NP>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
-  yw_units<1, 3, L, JW, NP>(sX, sW, lane, rb[1], rb[2], ar, ai);        // singles
+  const int* rb = (nw == 4 ? cYRowW4 : cYRowW12) + rid * (2 * nw + 1) + 2 * w;
+  yw_units<2, kYPairU, L, JW, NP, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
+  yw_units<1, 3, L, JW, NP, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);        // singles
 #pragma unroll
   for (int m = 0; m < L; ++m) {
     sred[((w * (T + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
     sred[((w * (T + 1) + m) * 2 + 1) * 32 + lane] = ai[m];
   }
-  __syncthreads();
+  group_sync<GR>(g);
   const int hb = c_half_off(J) + mb * (J + 1);
   const int fb = kXPad + c_full_off(J) + mb * (J + 1);
   for (int ma = w; ma <= J; ma += nw) {
@@ -1111,11 +1137,12 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
     }
     reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
   }
-  __syncthreads();
+  group_sync<GR>(g);
 }
 
-template <int T>
+template <int T, int GR>
 __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs A) {
+  constexpr int kYGW = kYWarps / GR;
   constexpr int NF = c_full_off(T + 1);
   constexpr int NP = NF + 2 * kXPad;
   constexpr int NH = c_half_off(T + 1);
@@ -1124,6 +1151,11 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   double* sred = smem + 2 * NP * 32;  // [warp][T+1][re|im][32]
   double* sW = sred + kYWarps * (T + 1) * 2 * 32;  // W per item
   __shared__ double se[kYWarps][32];
+#ifdef SNAP_Y_PROFILE
+  const long long t_start = clock64();
+  unsigned long long g_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+#endif
   for (int e = threadIdx.x; e < A.nitems; e += blockDim.x) sW[e] = __ldg(A.itw + e);
   const int tile = blockIdx.x;
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
@@ -1167,9 +1199,19 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
+  const int g = w / kYGW, wg = w - g * kYGW;
+  const int* tasks = A.tasks + (size_t)(blockIdx.y * GR + g) * A.task_cap;
+  double* sredg = sred + (size_t)g * kYGW * (T + 1) * 2 * 32;
   double* Yt = A.Y + (size_t)(tile * 32 + lane) * NH * 2;  // Y' atom-major, interleaved complex
   double e_acc = 0.0;
+#ifdef SNAP_Y_PROFILE
+  long long t_prev = clock64();
+  if (threadIdx.x == 0 && A.prof) {  // [60]: prologue, [61]: CTA count, [62]: CTA total
+    atomicAdd(reinterpret_cast<unsigned long long*>(A.prof) + 60,
+              (unsigned long long)(t_prev - t_start));
+    atomicAdd(reinterpret_cast<unsigned long long*>(A.prof) + 61, 1ull);
+  }
+#endif
   for (int q = 0;; ++q) {
     const int code = __ldg(tasks + q);
     if (code < 0) break;
@@ -1178,8 +1220,8 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
 #define YWROW(JJ)                                                                       \
   case JJ:                                                                              \
     if constexpr (JJ <= T) {                                                            \
-      if (2 * mb == JJ) yw_row<T, JJ, true>(sX, sred, sW, lane, w, nw, mb, rid, A, Yt, e_acc); \
-      else yw_row<T, JJ, false>(sX, sred, sW, lane, w, nw, mb, rid, A, Yt, e_acc);          \
+      if (2 * mb == JJ) yw_row<T, JJ, true, GR>(sX, sredg, sW, lane, g, wg, mb, rid, A, Yt, e_acc); \
+      else yw_row<T, JJ, false, GR>(sX, sredg, sW, lane, g, wg, mb, rid, A, Yt, e_acc);          \
     }                                                                                   \
     break;
     switch (j) {
@@ -1187,6 +1229,12 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
       default: break;
     }
 #undef YWROW
+#ifdef SNAP_Y_PROFILE  // per-row cycle counts (cost-model calibration)
+    const long long t_now = clock64();
+    if (wg == 0 && lane == 0 && A.prof)
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.prof) + rid, (unsigned long long)(t_now - t_prev));
+    t_prev = t_now;
+#endif
   }
   se[w][lane] = e_acc;
   __syncthreads();
@@ -1195,6 +1243,21 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     for (int q = 0; q < nw; ++q) s += se[q][lane];
     const int atom = tile * 32 + lane;
     energy_epilogue(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
+#ifdef SNAP_Y_PROFILE
+    if (lane == 0 && A.prof) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(A.prof) + 62,
+                (unsigned long long)(clock64() - t_start));
+      unsigned long long g_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+      const int b = blockIdx.y * gridDim.x + blockIdx.x;
+      if (b < 1024) {  // [64 + 2b]: start, end (ns)
+        reinterpret_cast<unsigned long long*>(A.prof)[64 + 2 * b] = g_start;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        reinterpret_cast<unsigned long long*>(A.prof)[65 + 2 * b] = ((g_end - g_start) << 8) | smid;
+      }
+    }
+#endif
   }
 }
 

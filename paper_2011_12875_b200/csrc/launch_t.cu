@@ -91,18 +91,32 @@ void launch_Y_t(snapgpu_ctx* c) {
       a.V = c->d_V.p;
       a.Y = c->d_Y.p;
       a.expand = c->d_expand.p;
-      a.itw = c->d_citw.p;
-      a.nitems = static_cast<int>(c->ycplan.items.size());
+      a.itw = c->d_citw[c->y_groups == 3 ? 0 : 1].p;
+      a.nitems = static_cast<int>(c->ycplan[0].items.size());
+      a.prof = nullptr;
+#ifdef SNAP_Y_PROFILE
+      if (!g_yprof) {
+        CK(cudaMalloc(&g_yprof, 2112 * sizeof(long long)));
+        CK(cudaMemset(g_yprof, 0, 2112 * sizeof(long long)));
+      }
+      a.prof = g_yprof;
+#endif
       a.tasks = c->d_tasks.p;
       a.task_cap = c->task_cap;
       a.nlocal = c->nlocal;
       a.E = energy_out(c);
       const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYWarps * (T + 1) * 2 * 32 +
                                             (size_t)a.nitems);
-      CK(cudaFuncSetAttribute(k_compute_Y_cwin<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
       dim3 grid(c->ntiles, c->y_parts_used);
-      k_compute_Y_cwin<T><<<grid, kYWarps * 32, smem, c->stream>>>(a);
+      if (c->y_groups == 3) {
+        CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 3>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_compute_Y_cwin<T, 3><<<grid, kYWarps * 32, smem, c->stream>>>(a);
+      } else {
+        CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 1>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_compute_Y_cwin<T, 1><<<grid, kYWarps * 32, smem, c->stream>>>(a);
+      }
       CK(cudaGetLastError());
       return;
     }
@@ -161,12 +175,16 @@ void upload_ytables_t(int device, const YTablesHost& t) {
     for (int d : done)
       if (d == device) return;
     require(t.cw.size() == (size_t)c_cw_total(T), "compute_Y: C' table size mismatch");
-    require(t.items.size() <= (size_t)kYItemCap, "compute_Y: item table exceeds constant bank");
-    require(t.rw_begin.size() == (size_t)c_acc_off(T + 1) * (2 * kYWarps + 1),
+    require(t.items4.size() <= (size_t)kYItemCap && t.items12.size() <= (size_t)kYItemCap,
+            "compute_Y: unit table exceeds constant bank");
+    require(t.rw4.size() == (size_t)c_acc_off(T + 1) * (2 * 4 + 1) &&
+                t.rw12.size() == (size_t)c_acc_off(T + 1) * (2 * 12 + 1),
             "compute_Y: row/warp table size mismatch");
     CK(cudaMemcpyToSymbol(cCW, t.cw.data(), t.cw.size() * sizeof(double)));
-    CK(cudaMemcpyToSymbol(cYItems, t.items.data(), t.items.size() * sizeof(uint4)));
-    CK(cudaMemcpyToSymbol(cYRowW, t.rw_begin.data(), t.rw_begin.size() * sizeof(int)));
+    CK(cudaMemcpyToSymbol(cYItems4, t.items4.data(), t.items4.size() * sizeof(uint4)));
+    CK(cudaMemcpyToSymbol(cYItems12, t.items12.data(), t.items12.size() * sizeof(uint4)));
+    CK(cudaMemcpyToSymbol(cYRowW4, t.rw4.data(), t.rw4.size() * sizeof(int)));
+    CK(cudaMemcpyToSymbol(cYRowW12, t.rw12.data(), t.rw12.size() * sizeof(int)));
     done.push_back(device);
   }
 #else

@@ -79,7 +79,12 @@ void plan_y(snapgpu_ctx* c) {
     // one CTA per SM: never exceed a single wave
     if (parts <= 0) parts = std::max(1, std::min(8, nsm / std::max(1, c->ntiles)));
     c->y_parts_used = parts;
-    std::vector<int> tasks = y_row_schedule(c->maps, c->ycplan.row_cost, parts, &c->task_cap);
+    // one row list per (part, warp group): three 4-warp groups when a CTA
+    // owns a whole tile, one 12-warp group (finest row granularity) when the
+    // tile is split over several CTAs
+    c->y_groups = (parts == 1) ? 3 : 1;
+    std::vector<int> tasks =
+        y_row_schedule(c->maps, c->ycplan[0].row_cost, parts * c->y_groups, &c->task_cap);
     c->d_tasks.alloc(tasks.size());
     CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
     return;
@@ -101,10 +106,12 @@ void plan_y(snapgpu_ctx* c) {
 void upload_beta(snapgpu_ctx* c) {
   if (c->y_impl == 0) {
     const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
-    const std::vector<double> itw = ycoop_weights(c->ycplan, c->maps, W);
-    c->d_citw.alloc(std::max<size_t>(1, itw.size()));
-    CK(cudaMemcpy(c->d_citw.p, itw.data(), itw.size() * sizeof(double),
-                  cudaMemcpyHostToDevice));
+    for (int k = 0; k < 2; ++k) {  // item order of the 4- and 12-warp unit tables
+      const std::vector<double> itw = ycoop_weights(c->ycplan[k], c->maps, W);
+      c->d_citw[k].alloc(std::max<size_t>(1, itw.size()));
+      CK(cudaMemcpy(c->d_citw[k].p, itw.data(), itw.size() * sizeof(double),
+                    cudaMemcpyHostToDevice));
+    }
     return;
   }
   const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), true);
@@ -113,9 +120,8 @@ void upload_beta(snapgpu_ctx* c) {
   CK(cudaMemcpy(c->d_itw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
 }
 
-void build_ycoop(snapgpu_ctx* c) {
-  c->ycplan = ycoop_pair_plan(c->maps, kYWarps);
-  // constant-window units, packed for the constant bank (kernels.cuh cYItems)
+// constant-window units, packed for the constant bank (kernels.cuh cYItems4/12)
+static std::vector<uint4> pack_units(const snapgpu_ctx* c, const YCoopPlan& p) {
   std::vector<int> cwoff(c->maps.tuples.size());
   int o = 0;
   for (size_t q = 0; q < cwoff.size(); ++q) {
@@ -123,23 +129,32 @@ void build_ycoop(snapgpu_ctx* c) {
     o += (c->maps.tuples[q].j2 + 1) * (c->maps.tuples[q].j + 1);
   }
   auto rows = [&](int i) {  // x1 window base | x2 row base << 16 of item i
-    const Tuple& tp = c->maps.tuples[c->ycplan.items[i][0]];
+    const Tuple& tp = c->maps.tuples[p.items[i][0]];
     const int D = (tp.j1 + tp.j2 - tp.j) / 2;
-    const int mb1 = c->ycplan.items[i][1], mb2 = c->ycplan.items[i][2];
+    const int mb1 = p.items[i][1], mb2 = p.items[i][2];
     const unsigned x1 = c->maps.full_off[tp.j1] + mb1 * (tp.j1 + 1) + D;
     const unsigned x2 = c->maps.full_off[tp.j2] + mb2 * (tp.j2 + 1);
     return x1 | (x2 << 16);
   };
+  std::vector<uint4> out(p.units.size());
+  for (size_t u = 0; u < out.size(); ++u) {
+    const int i0 = p.units[u][0], n = p.units[u][1];
+    const Tuple& tp = c->maps.tuples[p.items[i0][0]];
+    out[u] = make_uint4(rows(i0), tp.j2 | (cwoff[p.items[i0][0]] << 8),
+                        rows(n == 2 ? i0 + 1 : i0), static_cast<unsigned>(i0));
+  }
+  return out;
+}
+
+void build_ycoop(snapgpu_ctx* c) {
+  c->ycplan[0] = ycoop_pair_plan(c->maps, 4);   // 4 warps per row (3 groups)
+  c->ycplan[1] = ycoop_pair_plan(c->maps, 12);  // 12 warps per row (1 group)
   YTablesHost t;
   t.cw = c->yplan.cw;
-  t.rw_begin = c->ycplan.rw_begin;
-  t.items.resize(c->ycplan.units.size());
-  for (size_t u = 0; u < t.items.size(); ++u) {
-    const int i0 = c->ycplan.units[u][0], n = c->ycplan.units[u][1];
-    const Tuple& tp = c->maps.tuples[c->ycplan.items[i0][0]];
-    t.items[u] = make_uint4(rows(i0), tp.j2 | (cwoff[c->ycplan.items[i0][0]] << 8),
-                            rows(n == 2 ? i0 + 1 : i0), static_cast<unsigned>(i0));
-  }
+  t.items4 = pack_units(c, c->ycplan[0]);
+  t.items12 = pack_units(c, c->ycplan[1]);
+  t.rw4 = c->ycplan[0].rw_begin;
+  t.rw12 = c->ycplan[1].rw_begin;
   upload_ytables(c->device, c->T, t);
   upload_beta(c);
 }
@@ -312,6 +327,17 @@ void run_direct(snapgpu_ctx* c) {
 // ===========================================================================
 // C-ABI
 // ===========================================================================
+#ifdef SNAP_Y_PROFILE
+long long* snapgpu::host::g_yprof = nullptr;
+extern "C" int snapgpu_debug_yprof(long long* out, int n) {
+  if (!g_yprof) return -1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, g_yprof, sizeof(long long) * n, cudaMemcpyDeviceToHost);
+  cudaMemset(g_yprof, 0, sizeof(long long) * 2112);
+  return 0;
+}
+#endif
+
 extern "C" {
 
 const char* snapgpu_last_error(const snapgpu_ctx* c) {
@@ -429,7 +455,8 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_items.release();
   c->d_rowbeg.release();
 
-  c->d_citw.release();
+  c->d_citw[0].release();
+  c->d_citw[1].release();
   c->d_expand.release();
   c->d_tasks.release();
   c->d_numneigh.release();

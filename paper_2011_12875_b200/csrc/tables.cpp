@@ -356,7 +356,15 @@ YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps) {
           tot += c;
         }
       }
-      p.row_cost.push_back(tot);
+      // Row costs for the row -> (part, warp group) schedule: at 2J = 8 the
+      // measured per-row cycles of k_compute_Y_cwin (tools/yprof.py on a
+      // B200, 256k atoms; the model misses the per-row and per-step
+      // overheads of the small-j rows), else the FP64 instruction model.
+      static const double kMeasured8[25] = {
+          11335, 6281,  23115, 20171, 16149, 23440, 32087, 37028, 29111, 23506, 28685, 30951, 34146,
+          45839, 43764, 32435, 25296, 31193, 35644, 45185, 37471, 47032, 50489, 59654, 39880};
+      const int rid = static_cast<int>(p.row_cost.size());
+      p.row_cost.push_back(m.T == 8 ? kMeasured8[rid] : tot);
       std::vector<std::vector<int>> buckets = lpt(costs, warps);
       int off = static_cast<int>(p.units.size());
       for (int w = 0; w < warps; ++w) {

@@ -1,0 +1,28 @@
+import ctypes as C, sys
+import numpy as np
+sys.path.insert(0, '.')
+import paper_2011_12875_b200 as snap
+p = snap.bcc_problem(10, 10, 10, twojmax=8)
+eng = snap.SnapEngine.for_problem(p); eng.set_problem(p); eng.enable_stage_timing(True)
+eng.run(); eng.synchronize()
+L = snap.library(); buf = (C.c_longlong * 2112)()
+L.snapgpu_debug_yprof(buf, 2112)
+eng.run(); eng.synchronize()
+L.snapgpu_debug_yprof(buf, 2112)
+a = np.array(buf[64:64 + 2 * 126], dtype=np.int64).reshape(-1, 2)
+smid = a[:, 1] & 255
+a[:, 1] = a[:, 0] + (a[:, 1] >> 8)
+t0 = a[:, 0].min()
+s = (a[:, 0] - t0) / 1e3; e = (a[:, 1] - t0) / 1e3
+print("start us: min %.1f med %.1f max %.1f" % (s.min(), np.median(s), s.max()))
+print("end   us: min %.1f med %.1f max %.1f" % (e.min(), np.median(e), e.max()))
+print("dur   us: min %.1f med %.1f max %.1f" % ((e - s).min(), np.median(e - s), (e - s).max()))
+print("stage times", eng.stage_times())
+d = e - s
+nx = 63
+for part in range(2):
+    dd = d[part * nx:(part + 1) * nx]
+    print("part", part, "dur us min %.1f med %.1f max %.1f" % (dd.min(), np.median(dd), dd.max()))
+order = np.argsort(-d)
+print("slowest CTAs (block, sm, start us, dur us):", [(int(i), int(smid[i]), round(float(s[i]), 1), round(float(d[i]), 1)) for i in order[:12]])
+print("fastest:", [(int(i), int(smid[i]), round(float(s[i]), 1), round(float(d[i]), 1)) for i in order[-6:]])
