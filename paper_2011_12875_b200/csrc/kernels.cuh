@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(UCfg<T>::WARPS * 32, SNAP_U_MINB)
 // compute_U, row-lane variant (2J <= 8)
 //
 // Lanes = (atom a, pair slot s, row r): a warp accumulates APW atoms at once,
-// each with SL pair slots (2 for large problems, 8 when the atoms are too few
+// each with SL pair slots (2 for large problems, 4 when the atoms are too few
 // to fill the SMs) of G row lanes (G = rows of the half level,
 // the fused-dE layout).  Lane r owns row mb = r of the current level (T+1
 // complex in registers) and advances it in place, v(t,r,c) = conj(a)

@@ -32,10 +32,14 @@ template <int T>
 void launch_U_t(snapgpu_ctx* c) {
   if constexpr (T <= 8) {
     if (c->u_impl == 0) {  // row-lane kernel
-      // two pair slots per atom when the atoms fill the SMs, else eight
+      // two pair slots per atom when the atoms fill the SMs, else four
+      // (measured at 2000 atoms: 2 / 4 / 8 slots -> 28.7 / 26.4 / 31.6 us)
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-      if (c->nlocal / U2Cfg<T, 2>::APW >= 8 * nsm) return launch_U2<T, 2>(c);
+      int sl = (c->nlocal / U2Cfg<T, 2>::APW >= 8 * nsm) ? 2 : 4;
+      if (const char* e = std::getenv("SNAPGPU_U_SLOTS")) sl = std::atoi(e);  // development A/B
+      if (sl == 2) return launch_U2<T, 2>(c);
+      if (sl == 4) return launch_U2<T, 4>(c);
       return launch_U2<T, 8>(c);
     }
   }
