@@ -1,0 +1,96 @@
+"""Full-size parity for BASELINE.json configs C3 (2J=8, 262,144 atoms) and C4
+(2J=14, 32,768 atoms), through checks whose cost does not grow with the size:
+
+* sampled atoms: the per-atom energy E_i and the pair gradients dE(i, k)
+  depend only on atom i's own neighbor list (compute_U snap_core.hpp:369-489,
+  compute_Y :1085-1200, compute_fused_dE :1274-1406), so the oracle run on a
+  sub-problem made of the sampled atoms' lists must reproduce the full-size
+  GPU values (every tile position, including the padded last tile);
+* Newton's third law on the closed periodic lattice: sum_i F_i = 0
+  (oracle.hpp:224-237);
+* determinism: a second run is bitwise identical (ordered reductions);
+* rotation invariance (oracle.hpp:175-203): energies invariant, forces
+  co-rotate with the displacements.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FTOL, ETOL = 1e-10, 1e-12
+
+
+def normerr(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def snap():
+    import paper_2011_12875_b200 as snap
+
+    return snap
+
+
+def _sample(n, k=48, seed=5):
+    rng = np.random.default_rng(seed)
+    idx = set(rng.choice(n, size=k - 4, replace=False).tolist())
+    idx.update([0, 31, n - 1, (n // 32) * 32 - 1])  # tile edges and the last atom
+    return np.array(sorted(i for i in idx if 0 <= i < n))
+
+
+def _subproblem(p, idx):
+    """The sampled atoms' own lists as a standalone problem (neighbor indices
+    remapped to valid non-self atoms: E_i and dE(i, k) do not depend on them)."""
+    from types import SimpleNamespace
+
+    m = len(idx)
+    S = p.nbr.shape[1]
+    nbr = (np.arange(m)[:, None] + 1 + np.arange(S)[None, :]) % m
+    return SimpleNamespace(twojmax=p.twojmax, rcut=p.rcut, rmin0=p.rmin0, rfac0=p.rfac0,
+                           wself=p.wself, self_flag=p.self_flag, beta=p.beta,
+                           weights=np.ones(1), numneigh=np.ascontiguousarray(p.numneigh[idx]),
+                           nbr=np.ascontiguousarray(nbr.astype(np.int32)),
+                           disp=np.ascontiguousarray(p.disp[idx]), types=None)
+
+
+@pytest.mark.parametrize("cells,T", [((64, 64, 32), 8), ((32, 32, 16), 14)],
+                         ids=["C3_2j8_262144", "C4_2j14_32768"])
+def test_full_size_sampled_atoms_vs_oracle(snap, port, cells, T):
+    p = snap.bcc_problem(*cells, twojmax=T)
+    n = p.natoms
+    eng = snap.SnapEngine.for_problem(p)
+    eng.set_problem(p)
+    eng.run()
+    f = eng.forces()
+    eatom, etot = eng.energy()
+    dedr = eng.dedr()
+    idx = _sample(n)
+    ref = port.run(_subproblem(p, idx), want=("eatom", "delist"))
+    assert normerr(eatom[idx], ref["eatom"]) <= ETOL
+    assert normerr(dedr[idx], ref["delist"]) <= FTOL
+    # closed periodic lattice: Newton's third law
+    assert np.abs(f.sum(axis=0)).max() <= 1e-12 * np.abs(f).max() * np.sqrt(n)
+    # total energy is the ordered sum of the per-atom energies
+    assert abs(etot - float(np.sum(eatom))) <= 1e-12 * abs(etot)
+    # determinism: bitwise equal energies on a second run
+    eng.run()
+    eatom2, etot2 = eng.energy()
+    assert etot2 == etot
+    assert np.array_equal(eatom2, eatom)
+    eng.close()
+
+
+def test_rotation_invariance_bcc2000(snap):
+    p = snap.bcc_problem(10, 10, 10, twojmax=8)
+    base = snap.run_pipeline(p)
+    rng = np.random.default_rng(7)
+    q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+    if np.linalg.det(q) < 0:
+        q[:, 0] = -q[:, 0]
+    pr = snap.Problem.from_any(p)
+    pr.disp = np.ascontiguousarray(p.disp @ q.T)
+    rot = snap.run_pipeline(pr)
+    assert normerr(rot.eatom, base.eatom) <= 1e-10
+    assert normerr(rot.forces, base.forces @ q.T) <= 1e-10
