@@ -130,6 +130,24 @@ int snapgpu_get_ulisttot(snapgpu_ctx* ctx, double* out);
 int snapgpu_get_ylist(snapgpu_ctx* ctx, double* out);
 int snapgpu_get_dedr(snapgpu_ctx* ctx, double* out);
 
+/* On-device neighbor lists: harness.hpp:119-202 built on
+ * the GPU from host positions (natoms x 3, any image) in an orthorhombic
+ * box[3]: strict r < Rcut, minimum image, lists sorted by index, stride =
+ * the largest count (<= 128).  Bitwise the lists of
+ * snapgpu_build_neighborlist; replaces snapgpu_set_neighbors (all atoms
+ * owned, one type).  snapgpu_get_neighbors reads them back. */
+int snapgpu_set_positions(snapgpu_ctx* ctx, int natoms, const double* pos,
+                          const double* box);
+int snapgpu_get_neighbors(snapgpu_ctx* ctx, int* numneigh, int* nbr, double* disp);
+
+/* Virial of the owned pairs from dElist (the paper keeps
+ * dElist for it): out6 = W_xx, W_yy, W_zz, W_xy, W_xz, W_yz
+ * with W_ab = sum_{i,k} r_ik,a f_ik,b, r_ik the center -> neighbor
+ * displacement and f_ik = -dE(i,k) the force on the neighbor
+ * (scatter_forces, snap_core.hpp:889-898).  Deterministic reduction; no
+ * reference equivalent (checked against dElist from the oracle). */
+int snapgpu_get_virial(snapgpu_ctx* ctx, double* out6);
+
 /* Device pointers for collectives (valid until the next set_neighbors):
  * forces natoms_total x 3, eatom nlocal, etotal 1. */
 int snapgpu_device_outputs(snapgpu_ctx* ctx, double** forces, double** eatom,

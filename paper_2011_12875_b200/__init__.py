@@ -88,6 +88,9 @@ def library() -> C.CDLL:
     L.snapgpu_get_ulisttot.argtypes = [vp, vp]
     L.snapgpu_get_ylist.argtypes = [vp, vp]
     L.snapgpu_get_dedr.argtypes = [vp, vp]
+    L.snapgpu_get_virial.argtypes = [vp, vp]
+    L.snapgpu_set_positions.argtypes = [vp, ip, vp, vp]
+    L.snapgpu_get_neighbors.argtypes = [vp, vp, vp, vp]
     L.snapgpu_device_outputs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
     L.snapgpu_get_forces_device.argtypes = [vp, vp]
     L.snapgpu_get_energy_device.argtypes = [vp, vp, vp]
@@ -359,6 +362,35 @@ class SnapEngine:
         o = np.zeros((self.nlocal, nh, 2), np.float64)
         self._c(self._L.snapgpu_get_ylist(self._h, o.ctypes.data))
         return o.view(np.complex128)[..., 0]
+
+    def set_positions(self, positions, box):
+        """Build the neighbor lists on the GPU from positions (SURVEY §8(f) F1;
+        harness.hpp:119-202, bitwise the host builder's lists)."""
+        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+        bx = np.ascontiguousarray(np.broadcast_to(np.asarray(box, np.float64), (3,)))
+        self._c(self._L.snapgpu_set_positions(self._h, int(pos.shape[0]), pos.ctypes.data,
+                                              bx.ctypes.data))
+        self.nlocal = self.natoms_total = int(pos.shape[0])
+        self.stride = int(self.neighbors(counts_only=True).max(initial=0))
+        return self
+
+    def neighbors(self, counts_only=False):
+        """(numneigh, nbr, disp) of the current lists, read back from the device."""
+        nn = np.zeros(self.nlocal, np.int32)
+        if counts_only:
+            self._c(self._L.snapgpu_get_neighbors(self._h, nn.ctypes.data, None, None))
+            return nn
+        nbr = np.zeros((self.nlocal, self.stride), np.int32)
+        disp = np.zeros((self.nlocal, self.stride, 3), np.float64)
+        self._c(self._L.snapgpu_get_neighbors(self._h, nn.ctypes.data, nbr.ctypes.data,
+                                              disp.ctypes.data))
+        return nn, nbr, disp
+
+    def virial(self) -> np.ndarray:
+        """W_xx, W_yy, W_zz, W_xy, W_xz, W_yz = sum_pairs r_ik (x) (-dE_ik)."""
+        o = np.zeros(6, np.float64)
+        self._c(self._L.snapgpu_get_virial(self._h, o.ctypes.data))
+        return o
 
     def dedr(self) -> np.ndarray:
         o = np.zeros((self.nlocal, self.stride, 3), np.float64)

@@ -103,6 +103,9 @@ struct snapgpu_ctx {
   // device arrays
   snapgpu::host::DevBuf<int> d_numneigh, d_nbr, d_types;
   snapgpu::host::DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal, d_part;
+  snapgpu::host::DevBuf<double> d_virial;  // virial partial sums + result
+  snapgpu::host::DevBuf<double> d_nlpos;   // device neighbor-list build: positions, wrapped
+  snapgpu::host::DevBuf<int> d_nlint;      // cell_of | members | counts | head | fill | max
   snapgpu::host::DevBuf<unsigned> d_ticket;
   snapgpu::host::DevBuf<unsigned> d_err;  // device validation flags (kErr*)
   unsigned* h_err = nullptr;              // pinned readback of d_err

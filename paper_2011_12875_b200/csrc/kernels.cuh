@@ -1739,6 +1739,211 @@ __global__ void __launch_bounds__(256) k_scatter_forces(const ScatterArgs A) {
   atomicAdd(fj + 2, -d2);
 }
 
+// ===========================================================================
+// Virial from dElist (the paper keeps dElist for it,
+// PAPER.md:420-421): W_ab = sum_{i,k} r_ik,a f_ik,b with r_ik the
+// displacement center -> neighbor and f_ik = -dE(i,k) the force the pair
+// exerts on the neighbor (scatter_forces, snap_core.hpp:889-898); components
+// xx, yy, zz, xy, xz, yz.  Per-CTA partial sums, then one CTA adds them in
+// block order: deterministic.
+// ===========================================================================
+struct VirialArgs {
+  const int* numneigh;
+  const double* disp;
+  const double* dedr;
+  int nlocal, stride;
+  double* part;  // [gridDim.x][6]
+  double* out;   // [6]
+};
+
+__global__ void __launch_bounds__(256) k_virial_partial(const VirialArgs A) {
+  __shared__ double red[6][256];
+  double v[6] = {0, 0, 0, 0, 0, 0};
+  const long n = (long)A.nlocal * A.stride;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < n;
+       p += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(p / A.stride), k = (int)(p - (long)i * A.stride);
+    if (k >= A.numneigh[i]) continue;
+    const double* r = A.disp + p * 3;
+    const double* d = A.dedr + p * 3;
+    v[0] -= r[0] * d[0];
+    v[1] -= r[1] * d[1];
+    v[2] -= r[2] * d[2];
+    v[3] -= r[0] * d[1];
+    v[4] -= r[0] * d[2];
+    v[5] -= r[1] * d[2];
+  }
+#pragma unroll
+  for (int c = 0; c < 6; ++c) red[c][threadIdx.x] = v[c];
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) A.part[blockIdx.x * 6 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void k_virial_final(const double* part, int nblk, double* out) {
+  if (threadIdx.x < 6) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[b * 6 + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// ===========================================================================
+// On-device neighbor lists: harness.hpp:119-202 restated
+// for the device.  wrap_coord (:82-86), the cell binning and min_image (:88-90)
+// use explicitly rounded IEEE operations (no FMA contraction), so the
+// displacements are bitwise those of the host builder (tables.cpp
+// build_neighborlist); each list is sorted by neighbor index.
+// ===========================================================================
+struct NLArgs {
+  const double* pos;
+  int n;
+  double box[3];
+  double rc2;
+  int nc[3];
+  int cells;       // 1: 27-cell stencil, 0: all pairs (fewer than 3 cells)
+  double* w;       // wrapped positions [n][3]
+  int* cell_of;    // [n]
+  int* head;       // [ncell + 1] (counts, then exclusive offsets)
+  int* fill;       // [ncell]
+  int* members;    // [n]
+  int* numneigh;   // [n]
+  int* maxcount;   // [1]
+  int* nbr;        // [n][stride]      (pass 2)
+  double* disp;    // [n][stride][3]   (pass 2)
+  int stride;
+};
+
+__device__ __forceinline__ double nl_wrap(double x, double box) {
+  const double w = __dsub_rn(x, __dmul_rn(box, floor(__ddiv_rn(x, box))));
+  return w >= box ? __dsub_rn(w, box) : w;
+}
+__device__ __forceinline__ double nl_min_image(double d, double box) {
+  return __dsub_rn(d, __dmul_rn(box, rint(__ddiv_rn(d, box))));
+}
+
+__global__ void k_nl_bin(const NLArgs A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  int ci[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double w = nl_wrap(A.pos[i * 3 + d], A.box[d]);
+    A.w[i * 3 + d] = w;
+    const int idx = (int)__dmul_rn(w, __ddiv_rn((double)A.nc[d], A.box[d]));
+    ci[d] = idx >= A.nc[d] ? A.nc[d] - 1 : idx;
+  }
+  if (A.cells) {
+    const int c = (ci[2] * A.nc[1] + ci[1]) * A.nc[0] + ci[0];
+    A.cell_of[i] = c;
+    atomicAdd(A.head + c + 1, 1);
+  }
+}
+
+// exclusive offsets: head[c] = sum of counts of cells < c (one CTA)
+__global__ void __launch_bounds__(1024) k_nl_scan(int* head, int ncell, int* fill) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (ncell + nt - 1) / nt;
+  const int b = min(ncell, t * per), e = min(ncell, b + per);
+  int s = 0;
+  for (int c = b; c < e; ++c) s += head[c + 1];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int q = 0; q < nt; ++q) {
+      const int v = part[q];
+      part[q] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  int acc = part[t];
+  for (int c = b; c < e; ++c) {
+    const int v = head[c + 1];
+    head[c] = acc;  // head[c] read only by this thread (c in [b, e))
+    fill[c] = acc;
+    acc += v;
+  }
+  if (e == ncell && b < e) head[ncell] = acc;
+  if (ncell == 0 && t == 0) head[0] = 0;
+}
+
+__global__ void k_nl_members(const NLArgs A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n || !A.cells) return;
+  A.members[atomicAdd(A.fill + A.cell_of[i], 1)] = i;
+}
+
+// PASS 1: count (and max); PASS 2: collect, sort by index, write.
+template <int PASS>
+__global__ void __launch_bounds__(128) k_nl_lists(const NLArgs A) {
+  constexpr int kCap = 128;  // per-atom candidates held for the sort
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  const double xi = A.w[i * 3], yi = A.w[i * 3 + 1], zi = A.w[i * 3 + 2];
+  int cnt = 0;
+  int idx[PASS == 2 ? kCap : 1];
+  auto consider = [&](int k) {
+    const double dx = nl_min_image(__dsub_rn(A.w[k * 3], xi), A.box[0]);
+    const double dy = nl_min_image(__dsub_rn(A.w[k * 3 + 1], yi), A.box[1]);
+    const double dz = nl_min_image(__dsub_rn(A.w[k * 3 + 2], zi), A.box[2]);
+    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    if (r2 < A.rc2) {
+      if (PASS == 2 && cnt < kCap) idx[cnt] = k;
+      ++cnt;
+    }
+  };
+  if (A.cells) {
+    const int c = A.cell_of[i];
+    const int cx = c % A.nc[0], cy = (c / A.nc[0]) % A.nc[1], cz = c / (A.nc[0] * A.nc[1]);
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int ox = (cx + dx + A.nc[0]) % A.nc[0], oy = (cy + dy + A.nc[1]) % A.nc[1],
+                    oz = (cz + dz + A.nc[2]) % A.nc[2];
+          const int oc = (oz * A.nc[1] + oy) * A.nc[0] + ox;
+          for (int s = A.head[oc]; s < A.head[oc + 1]; ++s) {
+            const int k = A.members[s];
+            if (k != i) consider(k);
+          }
+        }
+  } else {
+    for (int k = 0; k < A.n; ++k)
+      if (k != i) consider(k);
+  }
+  if (PASS == 1) {
+    A.numneigh[i] = cnt;
+    atomicMax(A.maxcount, cnt);
+    return;
+  }
+  // insertion sort by neighbor index (harness.hpp: lists sorted by index)
+  const int m = min(cnt, kCap);
+  for (int a = 1; a < m; ++a) {
+    const int v = idx[a];
+    int b = a - 1;
+    while (b >= 0 && idx[b] > v) {
+      idx[b + 1] = idx[b];
+      --b;
+    }
+    idx[b + 1] = v;
+  }
+  for (int q = 0; q < m; ++q) {
+    const int k = idx[q];
+    const size_t pk = (size_t)i * A.stride + q;
+    A.nbr[pk] = k;
+    A.disp[pk * 3 + 0] = nl_min_image(__dsub_rn(A.w[k * 3], xi), A.box[0]);
+    A.disp[pk * 3 + 1] = nl_min_image(__dsub_rn(A.w[k * 3 + 1], yi), A.box[1]);
+    A.disp[pk * 3 + 2] = nl_min_image(__dsub_rn(A.w[k * 3 + 2], zi), A.box[2]);
+  }
+}
+
 // Deterministic total energy: one CTA, fixed-order tree over eatom.
 __global__ void __launch_bounds__(1024) k_energy_total(const double* eatom, int n, double* out) {
   __shared__ double red[1024];

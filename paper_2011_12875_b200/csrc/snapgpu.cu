@@ -212,12 +212,13 @@ const char* device_error_message(unsigned f) {
 // (snapgpu_run_host reads the flags back with the results).
 void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int stride,
                const int* numneigh, const int* nbr, const double* disp, const int* types,
-               bool host_validate = true) {
+               bool host_validate = true, bool upload = true) {
   require(natoms_total >= 0 && nlocal >= 0 && atom_lo >= 0 && atom_lo + nlocal <= natoms_total,
           "problem: owned range outside the atom count");
   require(nlocal == 0 || natoms_total > 0, "problem: no atoms");
   require(stride >= 0, "problem: negative neighbor stride");
-  require(nlocal == 0 || stride == 0 || (numneigh && nbr && disp), "problem: null neighbor arrays");
+  require(!upload || nlocal == 0 || stride == 0 || (numneigh && nbr && disp),
+          "problem: null neighbor arrays");
   c->have_lists = c->have_U = c->have_Y = c->have_dE = false;
   const bool reshape = natoms_total != c->natoms_total || nlocal != c->nlocal ||
                        stride != c->stride || atom_lo != c->atom_lo ||
@@ -260,7 +261,7 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
   // Enqueue the uploads first (asynchronous from pinned memory) and validate
   // on the host while they are in flight; a failed validation leaves the
   // context without lists, so nothing runs on the uploaded data.
-  if (nlocal > 0) {
+  if (nlocal > 0 && upload) {
     CK(cudaMemcpyAsync(c->d_numneigh.p, numneigh, sizeof(int) * nlocal, cudaMemcpyHostToDevice,
                        c->stream));
     if (nslots > 0) {
@@ -456,6 +457,9 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_rowbeg.release();
 
   c->d_citw[0].release();
+  c->d_nlpos.release();
+  c->d_nlint.release();
+  c->d_virial.release();
   c->d_citw[1].release();
   c->d_expand.release();
   c->d_tasks.release();
@@ -708,6 +712,109 @@ int snapgpu_get_ylist(snapgpu_ctx* c, double* out) {
         }
       }
     }
+  });
+}
+
+int snapgpu_set_positions(snapgpu_ctx* c, int natoms, const double* pos, const double* box) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    require(natoms >= 0 && (natoms == 0 || pos) && box, "set_positions: bad arguments");
+    const double rcut = c->gp.rcut;
+    NLArgs a{};
+    for (int d = 0; d < 3; ++d) {  // harness.hpp:119-125 preconditions
+      require(box[d] > 0.0 && rcut > 0.0, "build_neighborlist: box and Rcut must be positive");
+      require(rcut <= 0.5 * box[d], "build_neighborlist: Rcut must not exceed box/2");
+      a.box[d] = box[d];
+      a.nc[d] = static_cast<int>(std::floor(box[d] / rcut));
+    }
+    a.cells = (a.nc[0] >= 3 && a.nc[1] >= 3 && a.nc[2] >= 3) ? 1 : 0;
+    a.n = natoms;
+    a.rc2 = rcut * rcut;
+    const long ncell = a.cells ? (long)a.nc[0] * a.nc[1] * a.nc[2] : 0;
+    c->d_nlpos.alloc(std::max<size_t>(1, (size_t)natoms * 6));
+    c->d_nlint.alloc((size_t)std::max(1, natoms) * 3 + 2 * (size_t)ncell + 4);
+    double* dpos = c->d_nlpos.p;
+    a.pos = dpos;
+    a.w = dpos + (size_t)natoms * 3;
+    int* ib = c->d_nlint.p;
+    a.cell_of = ib;
+    a.members = ib + natoms;
+    a.numneigh = ib + 2 * (size_t)natoms;
+    a.head = ib + 3 * (size_t)natoms;
+    a.fill = a.head + ncell + 1;
+    a.maxcount = a.fill + ncell;
+    CK(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * natoms, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(a.head, 0, sizeof(int) * (ncell + 1), c->stream));
+    CK(cudaMemsetAsync(a.maxcount, 0, sizeof(int), c->stream));
+    const int blk = (natoms + 127) / 128;
+    if (natoms > 0) {
+      k_nl_bin<<<blk, 128, 0, c->stream>>>(a);
+      if (a.cells) {
+        k_nl_scan<<<1, 1024, 0, c->stream>>>(a.head, (int)ncell, a.fill);
+        k_nl_members<<<blk, 128, 0, c->stream>>>(a);
+      }
+      k_nl_lists<1><<<blk, 128, 0, c->stream>>>(a);
+      CK(cudaGetLastError());
+    }
+    int mx = 0;
+    CK(cudaMemcpyAsync(&mx, a.maxcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    require(mx <= 128, "set_positions: more than 128 neighbors within Rcut");
+    // shapes/allocations of the context (nothing uploaded: the lists are built in place)
+    set_lists(c, natoms, 0, natoms, mx, nullptr, nullptr, nullptr, nullptr, false, false);
+    a.nbr = c->d_nbr.p;
+    a.disp = c->d_disp.p;
+    a.stride = mx;
+    if (natoms > 0) {
+      CK(cudaMemcpyAsync(c->d_numneigh.p, a.numneigh, sizeof(int) * natoms,
+                         cudaMemcpyDeviceToDevice, c->stream));
+      if (mx > 0) {
+        CK(cudaMemsetAsync(c->d_nbr.p, 0, sizeof(int) * (size_t)natoms * mx, c->stream));
+        CK(cudaMemsetAsync(c->d_disp.p, 0, sizeof(double) * (size_t)natoms * mx * 3, c->stream));
+        k_nl_lists<2><<<blk, 128, 0, c->stream>>>(a);
+        CK(cudaGetLastError());
+      }
+    }
+  });
+}
+
+int snapgpu_get_neighbors(snapgpu_ctx* c, int* numneigh, int* nbr, double* disp) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_lists, "get_neighbors: no neighbor lists");
+    const size_t n = (size_t)c->nlocal, ns = n * c->stride;
+    if (numneigh && n)
+      CK(cudaMemcpyAsync(numneigh, c->d_numneigh.p, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                         c->stream));
+    if (nbr && ns)
+      CK(cudaMemcpyAsync(nbr, c->d_nbr.p, sizeof(int) * ns, cudaMemcpyDeviceToHost, c->stream));
+    if (disp && ns)
+      CK(cudaMemcpyAsync(disp, c->d_disp.p, sizeof(double) * ns * 3, cudaMemcpyDeviceToHost,
+                         c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int snapgpu_get_virial(snapgpu_ctx* c, double* out6) {
+  if (!c || !out6) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_dE, "get_virial before the force pass");
+    constexpr int kBlk = 148;
+    c->d_virial.alloc(kBlk * 6 + 6);
+    VirialArgs a;
+    a.numneigh = c->d_numneigh.p;
+    a.disp = c->d_disp.p;
+    a.dedr = c->d_dedr.p;
+    a.nlocal = c->nlocal;
+    a.stride = c->stride;
+    a.part = c->d_virial.p;
+    a.out = c->d_virial.p + kBlk * 6;
+    k_virial_partial<<<kBlk, 256, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+    k_virial_final<<<1, 32, 0, c->stream>>>(a.part, kBlk, a.out);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out6, a.out, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 
