@@ -197,11 +197,28 @@ __host__ __device__ constexpr double mirror_R(int t) {
 #ifndef SNAP_U_MINB
 #define SNAP_U_MINB 1
 #endif
+// Read-only tables of the later stages (compute_Y's constant bank, item
+// weights) that compute_U pulls into L2 while it runs, so the first
+// compute_Y warps do not take their constant-cache misses to HBM.
+struct L2Prefetch {
+  const char* p[4];
+  int bytes[4];
+};
+
 struct UArgs {
   PairArgs pr;
   GeoParams gp;
   double* V;  // [tile][2][NH][32]
+  L2Prefetch pf;
 };
+
+__device__ __forceinline__ void l2_prefetch(const L2Prefetch& P) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    for (int off = t * 128; off < P.bytes[r]; off += nt * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(P.p[r] + off));
+}
 
 template <int T>
 struct UCfg {
@@ -446,6 +463,7 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int S = A.pr.stride;
   const int i0 = (blockIdx.x * C::WARPS + w) * C::APW;  // first atom of the warp
+  l2_prefetch(A.pf);
   if (A.pr.types) {  // type range of every atom (grid-strided)
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < A.pr.natoms_total;
          a += gridDim.x * blockDim.x) {

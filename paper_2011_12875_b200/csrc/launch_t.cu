@@ -12,6 +12,32 @@
 namespace snapgpu {
 namespace host {
 
+// compute_Y's read-only tables, prefetched into L2 by compute_U
+template <int T>
+static L2Prefetch y_prefetch(snapgpu_ctx* c) {
+  L2Prefetch P{};
+#if SNAP_T <= 8
+  if (c->y_impl == 0) {
+    void* a[4] = {nullptr, nullptr, nullptr, nullptr};
+    CK(cudaGetSymbolAddress(&a[0], cCW));
+    CK(cudaGetSymbolAddress(&a[1], cYItems4));
+    CK(cudaGetSymbolAddress(&a[2], cYItems12));
+    const int g = c->y_groups == 3 ? 0 : 1;
+    a[3] = c->d_citw[g].p;
+    const int b[4] = {(int)sizeof(cCW), (int)(c->ycplan[0].units.size() * sizeof(uint4)),
+                      (int)(c->ycplan[1].units.size() * sizeof(uint4)),
+                      (int)(c->ycplan[g].items.size() * sizeof(double))};
+    for (int r = 0; r < 4; ++r) {
+      P.p[r] = static_cast<const char*>(a[r]);
+      P.bytes[r] = a[r] ? b[r] : 0;
+    }
+  }
+#else
+  (void)c;
+#endif
+  return P;
+}
+
 template <int T, int SL>
 static void launch_U2(snapgpu_ctx* c) {
   using C2 = U2Cfg<T, SL>;
@@ -19,6 +45,7 @@ static void launch_U2(snapgpu_ctx* c) {
   a.pr = pair_args(c);
   a.gp = c->gp;
   a.V = c->d_V.p;
+  a.pf = y_prefetch<T>(c);
   const size_t smem = sizeof(double) * (size_t)C2::WARPS * C2::APW * c->stride * 5;
   CK(cudaFuncSetAttribute(k_compute_U2<T, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::max<size_t>(smem, 48 * 1024)));
@@ -48,6 +75,7 @@ void launch_U_t(snapgpu_ctx* c) {
   a.pr = pair_args(c);
   a.gp = c->gp;
   a.V = c->d_V.p;
+  a.pf = L2Prefetch{};
   const size_t smem = sizeof(double) * ((size_t)C::WARPS * c->stride * 5 +
                                         (C::REGACC ? 0 : (size_t)C::WARPS * 2 * C::NACC * 32));
   static bool attr = false;

@@ -50,3 +50,6 @@ print("fit cycles = %.3f*model + %.1f*units + %.1f" % tuple(coef))
 print("total cycles per tile (all groups)", cyc.sum())
 nct = buf[61]
 print("CTAs", nct / reps, "prologue cycles/CTA", buf[60] / max(1, nct), "CTA total cycles/CTA", buf[62] / max(1, nct))
+ph = np.array(buf[40:44], dtype=float)
+print("row phases (warp-cycles, share): units %.1f%%  wait1 %.1f%%  reduce+store %.1f%%  wait2 %.1f%%" %
+      tuple(100 * ph / ph.sum()))
