@@ -857,13 +857,15 @@ __device__ __forceinline__ void y_row(const double* __restrict__ sV, double* __r
   __syncthreads();
 }
 
+constexpr int kYWinWarps = 12;  // max warps per k_compute_Y CTA
+
 template <int T, int TA>
-__global__ void __launch_bounds__(256) k_compute_Y(const YArgs A) {
+__global__ void __launch_bounds__(kYWinWarps * 32) k_compute_Y(const YArgs A) {
   constexpr int NH = c_half_off(T + 1);
   extern __shared__ double smem[];
   double* sV = smem;                   // [re|im][half idx][TA atoms]
   double* sred = smem + 2 * NH * TA;   // [warp][T+1][re|im][32]
-  __shared__ double se[8][32];
+  __shared__ double se[kYWinWarps][32];
   const int atom0 = blockIdx.x * TA;
   const double* Vt = A.V + (size_t)(atom0 >> 5) * 2 * NH * 32 + (atom0 & 31);
   for (int e = threadIdx.x; e < 2 * NH * TA; e += blockDim.x) {

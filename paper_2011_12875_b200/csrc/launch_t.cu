@@ -154,7 +154,7 @@ void launch_Y_t(snapgpu_ctx* c) {
     }
   }
 #endif
-  constexpr int RED = 8 * (T + 1) * 2 * 32 * 8;
+  constexpr int RED = kYWinWarps * (T + 1) * 2 * 32 * 8;
   if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
     if (c->y_ta == 32) return launch_Y_window<T, 32>(c);
   }

@@ -432,7 +432,11 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     }
     const int nh = c->maps.nhalf;
     // V tile + the cross-warp row buffer (8 warps) must fit in shared memory
-    const double red = 8.0 * (twojmax + 1) * 2 * 32 * 8;
+    // half-V window kernel (2J > 8): 12 warps per CTA (measured at 2J=14,
+    // 32k atoms: 4 / 6 / 8 warps -> 105 / 83 / 66 ms); the V tile + the
+    // cross-warp row buffer must fit in shared memory
+    if (c->y_impl != 0) c->y_warps = kYWinWarps;
+    const double red = (double)kYWinWarps * (twojmax + 1) * 2 * 32 * 8;
     c->y_ta_max = (2.0 * nh * 32 * 8 + red <= 200.0 * 1024) ? 32
                   : ((2.0 * nh * 16 * 8 + red <= 200.0 * 1024) ? 16 : 8);
     *out = c;
@@ -918,8 +922,9 @@ int snapgpu_stage_times(snapgpu_ctx* c, float* out4) {
 int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int y_tile_atoms) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    require(c->y_impl == 0 ? (y_warps == 0 || y_warps == kYWarps) : (y_warps >= 0 && y_warps <= 8),
-            "tune: y_warps must be 12 (2J <= 8) or in [0,8]");
+    require(c->y_impl == 0 ? (y_warps == 0 || y_warps == kYWarps)
+                           : (y_warps >= 0 && y_warps <= kYWinWarps),
+            "tune: y_warps must be 12 (2J <= 8) or in [0,12]");
     require(y_tile_atoms == 0 || y_tile_atoms == 8 || y_tile_atoms == 16 || y_tile_atoms == 32,
             "tune: y_tile_atoms in {0, 8, 16, 32}");
     if (y_warps > 0) c->y_warps = y_warps;
