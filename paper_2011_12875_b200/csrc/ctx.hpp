@@ -88,7 +88,11 @@ struct snapgpu_ctx {
   snapgpu::host::DevBuf<int> d_rowbeg, d_tasks, d_expand;
   snapgpu::YPlan yplan;
   snapgpu::YCoopPlan ycplan[2];  // constant-window units for 4 / 12 warps per row
-  int y_impl = 0;  // 0: constant-window (2J <= 8), 2: half-storage window
+  snapgpu::YQuadPlan yqplan;     // quad units (2J > 8)
+  snapgpu::host::DevBuf<int4> d_qunits;
+  snapgpu::host::DevBuf<double> d_qitw;
+  snapgpu::host::DevBuf<int> d_qrw, d_qrows;
+  int y_impl = 0;  // 0: constant-window (2J <= 8), 3: quad units (2J > 8), 2: half-V window
   int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
   int u_impl = 0;   // 0: row-lane compute_U (2J <= 8), 1: column-lane compute_U
   int task_cap = 0;

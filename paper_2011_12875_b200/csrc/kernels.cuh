@@ -908,6 +908,216 @@ __global__ void __launch_bounds__(kYWinWarps * 32) k_compute_Y(const YArgs A) {
   }
 }
 
+
+// ===========================================================================
+// compute_Y for 2J > 8, quad-unit variant.  The constant-window design of
+// k_compute_Y_cwin (full mirrored X tile in shared memory: no index clamps,
+// no sign flips) with an 8-atom tile (the 2J=14 X tile is 162 KB): lane =
+// (item slot q = lane/8, atom a = lane%8).  A unit is up to 4 items of one
+// (tuple, target row) — consecutive mb1 — so the 4 lane groups run the same
+// loop with the same C' coefficient at every step (one warp-uniform load)
+// and their partial rows are combined by two xor-shuffles.  12 warps share
+// each target row (LPT over units), partial rows meet in shared memory.
+// ===========================================================================
+constexpr int kQPad = 16;  // X pad: window reads reach J2+1 <= 15 below, D <= 14 above
+constexpr int kQWarps = 12;
+
+struct YQArgs {
+  const double* V;
+  double* Y;
+  const int* expand;   // half -> full scatter map
+  const int4* units;   // {x1_0 | x2_0 << 16, J2 | J1 << 8 | count << 16, C' offset, item0}
+  const double* itw;   // W per item (beta-dependent)
+  const int* rw;       // [row][kQWarps + 1] unit ranges
+  const double* cw;    // windowed C' (global; L1-resident)
+  const int* rows;     // row codes j*64+mb in processing order, -1 terminated
+  int nlocal;
+  EnergyOut E;
+};
+
+template <int T, int J, bool MID>
+__device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __restrict__ sred,
+                                       int lane, int w, int mb, int rid, const YQArgs& A,
+                                       double* __restrict__ Yt, double& e_acc) {
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int NP = NF + 2 * kQPad;
+  constexpr int L = MID ? J / 2 + 1 : J + 1;
+  constexpr int JW = J + 1;
+  constexpr int U = 2;
+  const int q = lane >> 3, a = lane & 7;
+  double ar[L], ai[L];
+#pragma unroll
+  for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
+  const int b = __ldg(A.rw + rid * (kQWarps + 1) + w), e = __ldg(A.rw + rid * (kQWarps + 1) + w + 1);
+  for (int it = b; it < e; ++it) {
+    const int4 u = __ldg(A.units + it);
+    const int J2 = u.y & 0xff, J1 = (u.y >> 8) & 0xff, cnt = u.y >> 16;
+    const bool act = q < cnt;
+    const int x1 = act ? (u.x & 0xffff) + q * (J1 + 1) : 0;
+    const int x2 = act ? (u.x >> 16) - q * (J2 + 1) : 0;
+    const double wt = act ? __ldg(A.itw + u.w + q) : 0.0;
+    const double* p1 = sX + (kQPad + x1) * 8 + a;  // x1[base + k] at p1[k*8]
+    const double* p2 = sX + (kQPad + x2) * 8 + a;
+    const double* c0 = A.cw + u.z;
+    double er[L + U - 1], ei[L + U - 1];
+#pragma unroll
+    for (int ma = 0; ma < L; ++ma) {
+      er[U - 1 + ma] = p1[ma * 8];
+      ei[U - 1 + ma] = p1[(NP + ma) * 8];
+    }
+    int a2 = 0;
+    for (; a2 + U - 1 <= J2; a2 += U) {
+#pragma unroll
+      for (int k = 1; k < U; ++k) {
+        er[U - 1 - k] = p1[(-a2 - k) * 8];
+        ei[U - 1 - k] = p1[(NP - a2 - k) * 8];
+      }
+#pragma unroll
+      for (int s = 0; s < U; ++s) {
+        const double x2r = wt * p2[(a2 + s) * 8], x2i = wt * p2[(NP + a2 + s) * 8];
+        const double* c = c0 + (a2 + s) * JW;
+#pragma unroll
+        for (int ma = 0; ma < L; ++ma) {
+          const double cc = __ldg(c + ma);
+          const double wr = er[U - 1 + ma - s], wi = ei[U - 1 + ma - s];
+          const double pr = fma(-wi, x2i, wr * x2r);
+          const double pi = fma(wi, x2r, wr * x2i);
+          ar[ma] = fma(cc, pr, ar[ma]);
+          ai[ma] = fma(cc, pi, ai[ma]);
+        }
+      }
+#pragma unroll
+      for (int ma = L - 1; ma >= 1; --ma) {
+        er[U - 1 + ma] = er[ma - 1];
+        ei[U - 1 + ma] = ei[ma - 1];
+      }
+      er[U - 1] = p1[(-a2 - U) * 8];
+      ei[U - 1] = p1[(NP - a2 - U) * 8];
+    }
+    for (; a2 <= J2; ++a2) {
+      const double x2r = wt * p2[a2 * 8], x2i = wt * p2[(NP + a2) * 8];
+      const double* c = c0 + a2 * JW;
+#pragma unroll
+      for (int ma = 0; ma < L; ++ma) {
+        const double cc = __ldg(c + ma);
+        const double pr = fma(-ei[U - 1 + ma], x2i, er[U - 1 + ma] * x2r);
+        const double pi = fma(ei[U - 1 + ma], x2r, er[U - 1 + ma] * x2i);
+        ar[ma] = fma(cc, pr, ar[ma]);
+        ai[ma] = fma(cc, pi, ai[ma]);
+      }
+#pragma unroll
+      for (int ma = L - 1; ma > 0; --ma) {
+        er[U - 1 + ma] = er[U - 2 + ma];
+        ei[U - 1 + ma] = ei[U - 2 + ma];
+      }
+      er[U - 1] = p1[(-a2 - 1) * 8];
+      ei[U - 1] = p1[(NP - a2 - 1) * 8];
+    }
+  }
+  // combine the four item slots, partial rows -> shared
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    ar[m] += __shfl_xor_sync(0xffffffffu, ar[m], 8);
+    ai[m] += __shfl_xor_sync(0xffffffffu, ai[m], 8);
+    ar[m] += __shfl_xor_sync(0xffffffffu, ar[m], 16);
+    ai[m] += __shfl_xor_sync(0xffffffffu, ai[m], 16);
+  }
+  if (q == 0) {
+#pragma unroll
+    for (int m = 0; m < L; ++m) {
+      sred[((w * (T + 1) + m) * 2 + 0) * 8 + a] = ar[m];
+      sred[((w * (T + 1) + m) * 2 + 1) * 8 + a] = ai[m];
+    }
+  }
+  __syncthreads();
+  constexpr int NH = c_half_off(T + 1);
+  const int hb = c_half_off(J) + mb * (J + 1);
+  const int fb = kQPad + c_full_off(J) + mb * (J + 1);
+  // stripes: warp w, lane group q -> output ma = w + kQWarps * q
+  const int ma = w + kQWarps * q;
+  if (ma <= J) {
+    double yr = 0.0, yi = 0.0;
+    if (ma < L) {
+      for (int s = 0; s < kQWarps; ++s) {
+        yr += sred[((s * (T + 1) + ma) * 2 + 0) * 8 + a];
+        yi += sred[((s * (T + 1) + ma) * 2 + 1) * 8 + a];
+      }
+      const double wgt = (MID && 2 * ma == J) ? 0.5 : 1.0;
+      yr *= wgt;
+      yi *= wgt;
+      e_acc += yr * sX[(fb + ma) * 8 + a] + yi * sX[(NP + fb + ma) * 8 + a];
+    }
+    reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
+  }
+  (void)NH;
+  __syncthreads();
+}
+
+template <int T>
+__global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs A) {
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int NP = NF + 2 * kQPad;
+  constexpr int NH = c_half_off(T + 1);
+  extern __shared__ double smem[];
+  double* sX = smem;                  // [re|im][pad | full idx | pad][8 atoms]
+  double* sred = smem + 2 * NP * 8;   // [warp][T+1][re|im][8]
+  __shared__ double se[kQWarps][32];
+  const int atom0 = blockIdx.x * 8;
+  for (int e = threadIdx.x; e < kQPad * 8; e += blockDim.x) {
+    sX[e] = sX[(kQPad + NF) * 8 + e] = 0.0;
+    sX[NP * 8 + e] = sX[(NP + kQPad + NF) * 8 + e] = 0.0;
+  }
+  const double* Vt = A.V + (size_t)(atom0 >> 5) * 2 * NH * 32 + (atom0 & 31);
+  for (int e = threadIdx.x; e < NH * 8; e += blockDim.x) {
+    const int h = e >> 3, a = e & 7;
+    const double re = __ldg(Vt + h * 32 + a), im = __ldg(Vt + (NH + h) * 32 + a);
+    const int2 sc = __ldg(reinterpret_cast<const int2*>(A.expand) + h);
+    sX[(kQPad + sc.x) * 8 + a] = re;
+    sX[(NP + kQPad + sc.x) * 8 + a] = im;
+    if (sc.y >= 0) {
+      const int fm = sc.y >> 1;
+      const bool neg = sc.y & 1;
+      sX[(kQPad + fm) * 8 + a] = neg ? -re : re;
+      sX[(NP + kQPad + fm) * 8 + a] = neg ? im : -im;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int a = lane & 7;
+  double* Yt = A.Y + (size_t)(atom0 + a) * NH * 2;
+  double e_acc = 0.0;
+  for (int q = 0;; ++q) {
+    const int code = __ldg(A.rows + q);
+    if (code < 0) break;
+    const int j = code >> 6, mb = code & 63;
+    const int rid = c_acc_off(j) + mb;
+#define YQROW(JJ)                                                                        \
+  case JJ:                                                                               \
+    if constexpr (JJ <= T) {                                                             \
+      if (2 * mb == JJ) yq_row<T, JJ, true>(sX, sred, lane, w, mb, rid, A, Yt, e_acc);   \
+      else yq_row<T, JJ, false>(sX, sred, lane, w, mb, rid, A, Yt, e_acc);               \
+    }                                                                                    \
+    break;
+    switch (j) {
+      YQROW(0) YQROW(1) YQROW(2) YQROW(3) YQROW(4) YQROW(5) YQROW(6) YQROW(7)
+      YQROW(8) YQROW(9) YQROW(10) YQROW(11) YQROW(12) YQROW(13) YQROW(14)
+      default: break;
+    }
+#undef YQROW
+  }
+  se[w][lane] = e_acc;
+  __syncthreads();
+  if (w == 0) {
+    double s = 0.0;
+    for (int q = 0; q < kQWarps; ++q) s += se[q][lane];
+    // lane (q, a) holds the stripes of item slot q: sum the four slots
+    s += __shfl_xor_sync(0xffffffffu, s, 8);
+    s += __shfl_xor_sync(0xffffffffu, s, 16);
+    const int atom = atom0 + a;
+    energy_epilogue(A.E, (2.0 / 3.0) * s, lane < 8 && atom < A.nlocal, atom);
+  }
+}
+
 // ===========================================================================
 // compute_Y, constant-window cooperative variant (2J <= 8)
 //

@@ -154,6 +154,29 @@ void launch_Y_t(snapgpu_ctx* c) {
     }
   }
 #endif
+  if constexpr (T > 8) {
+    if (c->y_impl == 3) {
+      constexpr int NF = c_full_off(T + 1);
+      constexpr int NP = NF + 2 * kQPad;
+      YQArgs a;
+      a.V = c->d_V.p;
+      a.Y = c->d_Y.p;
+      a.expand = c->d_expand.p;
+      a.units = c->d_qunits.p;
+      a.itw = c->d_qitw.p;
+      a.rw = c->d_qrw.p;
+      a.cw = c->d_cw.p;
+      a.rows = c->d_qrows.p;
+      a.nlocal = c->nlocal;
+      a.E = energy_out(c);
+      const size_t smem = sizeof(double) * (2 * NP * 8 + (size_t)kQWarps * (T + 1) * 2 * 8);
+      CK(cudaFuncSetAttribute(k_compute_Y_quad<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+      k_compute_Y_quad<T><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
   constexpr int RED = kYWinWarps * (T + 1) * 2 * 32 * 8;
   if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
     if (c->y_ta == 32) return launch_Y_window<T, 32>(c);

@@ -72,6 +72,7 @@ void upload_ytables(int device, int T, const YTablesHost& t) {
 void build_ycoop(snapgpu_ctx* c);
 
 void plan_y(snapgpu_ctx* c) {
+  if (c->y_impl == 3) return;  // quad-unit kernel: fixed row order, one CTA per 8 atoms
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
   if (c->y_impl == 0) {  // one 32-atom tile per CTA, all warps per row
@@ -112,6 +113,13 @@ void upload_beta(snapgpu_ctx* c) {
       CK(cudaMemcpy(c->d_citw[k].p, itw.data(), itw.size() * sizeof(double),
                     cudaMemcpyHostToDevice));
     }
+    return;
+  }
+  if (c->y_impl == 3) {
+    const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
+    const std::vector<double> itw = yquad_weights(c->yqplan, c->maps, W);
+    c->d_qitw.alloc(std::max<size_t>(1, itw.size()));
+    CK(cudaMemcpy(c->d_qitw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
     return;
   }
   const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), true);
@@ -414,7 +422,7 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     up(c->d_cw, c->yplan.cw);
     // compute_Y implementation: constant-window (default for 2J <= 8, where
     // the windowed C' fits constant memory), unrolled (2J = 8), half-V window.
-    c->y_impl = (cw_base(twojmax) >= 0) ? 0 : 2;
+    c->y_impl = (cw_base(twojmax) >= 0) ? 0 : 3;
     c->de_impl = 0;  // reverse mode at every 2J (2J=14: 4.2 ms vs 8.6 ms forward at 32k atoms)
     if (const char* e = std::getenv("SNAPGPU_DE_IMPL"))  // A/B switch for development
       c->de_impl = (std::string(e) == "forward") ? 1 : 0;
@@ -428,6 +436,17 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
       up(c->d_expand, half_scatter_map(c->maps));
       build_ycoop(c);  // constant-bank tables + the beta-dependent item weights
     } else {
+      if (c->y_impl == 3) {  // quad-unit tables (beta-independent part)
+        up(c->d_expand, half_scatter_map(c->maps));
+        c->yqplan = yquad_plan(c->maps, kQWarps);
+        std::vector<int4> u(c->yqplan.units.size());
+        for (size_t q = 0; q < u.size(); ++q)
+          u[q] = make_int4(c->yqplan.units[q][0], c->yqplan.units[q][1], c->yqplan.units[q][2],
+                           c->yqplan.units[q][3]);
+        up(c->d_qunits, u);
+        up(c->d_qrw, c->yqplan.rw);
+        up(c->d_qrows, c->yqplan.rows);
+      }
       upload_beta(c);
     }
     const int nh = c->maps.nhalf;
@@ -461,6 +480,10 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_rowbeg.release();
 
   c->d_citw[0].release();
+  c->d_qunits.release();
+  c->d_qitw.release();
+  c->d_qrw.release();
+  c->d_qrows.release();
   c->d_nlpos.release();
   c->d_nlint.release();
   c->d_virial.release();

@@ -384,6 +384,74 @@ YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps) {
   return p;
 }
 
+YQuadPlan yquad_plan(const IndexMaps& m, int warps) {
+  YQuadPlan p;
+  std::vector<int> cwoff(m.tuples.size());
+  int o = 0;
+  for (std::size_t q = 0; q < m.tuples.size(); ++q) {
+    cwoff[q] = o;
+    o += (m.tuples[q].j2 + 1) * (m.tuples[q].j + 1);
+  }
+  std::vector<std::pair<double, int>> rowcost;
+  for (int j = 0; j <= m.T; ++j)
+    for (int mb = 0; 2 * mb <= j; ++mb) {
+      const int nout = (2 * mb == j) ? j / 2 + 1 : j + 1;
+      std::vector<std::array<int, 4>> us;
+      std::vector<std::vector<std::array<int, 3>>> uit;
+      std::vector<std::pair<double, int>> costs;
+      double tot = 0.0;
+      for (std::size_t q = 0; q < m.tuples.size(); ++q) {
+        const Tuple& tp = m.tuples[q];
+        if (tp.j != j) continue;
+        const int D = (tp.j1 + tp.j2 - tp.j) / 2;
+        const int lo = std::max(0, mb + D - tp.j2), hi = std::min(tp.j1, mb + D);
+        for (int mb1 = lo; mb1 <= hi; mb1 += 4) {
+          const int cnt = std::min(4, hi - mb1 + 1);
+          std::vector<std::array<int, 3>> its;
+          for (int k = 0; k < cnt; ++k)
+            its.push_back({static_cast<int>(q), mb1 + k, mb + D - mb1 - k});
+          const int x1 = m.full_off[tp.j1] + mb1 * (tp.j1 + 1) + D;
+          const int x2 = m.full_off[tp.j2] + (mb + D - mb1) * (tp.j2 + 1);
+          us.push_back({x1 | (x2 << 16), tp.j2 | (tp.j1 << 8) | (cnt << 16), cwoff[q], 0});
+          uit.push_back(its);
+          const double c = (tp.j2 + 1) * (6.0 * nout + 24.0) + 60.0;
+          costs.push_back({c, static_cast<int>(us.size()) - 1});
+          tot += c;
+        }
+      }
+      rowcost.push_back({tot, j * 64 + mb});
+      std::vector<std::vector<int>> buckets = lpt(costs, warps);
+      int off = static_cast<int>(p.units.size());
+      for (int w = 0; w < warps; ++w) {
+        std::sort(buckets[w].begin(), buckets[w].end());
+        p.rw.push_back(off);
+        for (int idx : buckets[w]) {
+          std::array<int, 4> u = us[idx];
+          u[3] = static_cast<int>(p.items.size());
+          for (const auto& it : uit[idx]) p.items.push_back(it);
+          p.units.push_back(u);
+        }
+        off = static_cast<int>(p.units.size());
+      }
+      p.rw.push_back(off);
+    }
+  std::stable_sort(rowcost.begin(), rowcost.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  for (const auto& r : rowcost) p.rows.push_back(r.second);
+  p.rows.push_back(-1);
+  return p;
+}
+
+std::vector<double> yquad_weights(const YQuadPlan& p, const IndexMaps& m,
+                                  const std::vector<double>& wtab) {
+  std::vector<double> out(p.items.size());
+  for (std::size_t i = 0; i < p.items.size(); ++i) {
+    const Tuple& tp = m.tuples[p.items[i][0]];
+    out[i] = wtab[tp.cg_off + p.items[i][1] * (tp.j2 + 1) + p.items[i][2]];
+  }
+  return out;
+}
+
 std::vector<double> ycoop_weights(const YCoopPlan& p, const IndexMaps& m,
                                   const std::vector<double>& wtab) {
   std::vector<double> out(p.items.size());

@@ -105,6 +105,21 @@ YCoopPlan ycoop_plan(const IndexMaps& m, int warps, bool lpt_split);
 YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps);
 std::vector<double> ycoop_weights(const YCoopPlan& p, const IndexMaps& m,
                                   const std::vector<double>& wtab);
+// Quad units for the 2J > 8 compute_Y (kernels.cuh k_compute_Y_quad): per
+// target row, up to 4 consecutive mb1 items of one tuple form a unit (they
+// share every C' coefficient); units are LPT-split over `warps` warps.
+// unit = {x1_0 | x2_0 << 16, J2 | J1 << 8 | count << 16, C' offset, item0};
+// items = {tuple, mb1, mb2} (W order); rw = [row][warps + 1] unit ranges.
+struct YQuadPlan {
+  std::vector<std::array<int, 4>> units;
+  std::vector<std::array<int, 3>> items;
+  std::vector<int> rw;
+  std::vector<int> rows;  // row codes j*64+mb (decreasing cost), -1 terminated
+};
+YQuadPlan yquad_plan(const IndexMaps& m, int warps);
+std::vector<double> yquad_weights(const YQuadPlan& p, const IndexMaps& m,
+                                  const std::vector<double>& wtab);
+
 // LPT assignment of rows to workers: [worker][cap] row codes j*64+mb, -1 end.
 std::vector<int> y_row_schedule(const IndexMaps& m, const std::vector<double>& row_cost,
                                 int workers, int* cap);
