@@ -89,6 +89,7 @@ struct snapgpu_ctx {
   snapgpu::YPlan yplan;
   snapgpu::YCoopPlan ycplan[2];  // constant-window units for 4 / 12 warps per row
   snapgpu::YQuadPlan yqplan;     // quad units (2J > 8)
+  int yq_groups = 3;             // warp groups per quad-unit CTA (1 or 3)
   snapgpu::host::DevBuf<int4> d_qunits;
   snapgpu::host::DevBuf<double> d_qitw;
   snapgpu::host::DevBuf<int> d_qrw, d_qrows;

@@ -928,17 +928,28 @@ struct YQArgs {
   const int* expand;   // half -> full scatter map
   const int4* units;   // {x1_0 | x2_0 << 16, J2 | J1 << 8 | count << 16, C' offset, item0}
   const double* itw;   // W per item (beta-dependent)
-  const int* rw;       // [row][kQWarps + 1] unit ranges
+  const int* rw;       // [row][warps per group + 1] unit ranges
   const double* cw;    // windowed C' (global; L1-resident)
-  const int* rows;     // row codes j*64+mb in processing order, -1 terminated
+  const int* rows;     // [group][rows_cap] row codes j*64+mb, -1 terminated
+  int rows_cap;
   int nlocal;
   EnergyOut E;
 };
 
-template <int T, int J, bool MID>
+__device__ __forceinline__ void yq_sync(int g, int nthreads) {
+  if (nthreads == kQWarps * 32) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthreads) : "memory");
+  }
+}
+
+// GR groups of kQWarps/GR warps; g = group, w = warp within the group
+template <int T, int J, bool MID, int GR>
 __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __restrict__ sred,
-                                       int lane, int w, int mb, int rid, const YQArgs& A,
+                                       int lane, int g, int w, int mb, int rid, const YQArgs& A,
                                        double* __restrict__ Yt, double& e_acc) {
+  constexpr int NW = kQWarps / GR;
   constexpr int NF = c_full_off(T + 1);
   constexpr int NP = NF + 2 * kQPad;
   constexpr int L = MID ? J / 2 + 1 : J + 1;
@@ -948,7 +959,7 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
   double ar[L], ai[L];
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
-  const int b = __ldg(A.rw + rid * (kQWarps + 1) + w), e = __ldg(A.rw + rid * (kQWarps + 1) + w + 1);
+  const int b = __ldg(A.rw + rid * (NW + 1) + w), e = __ldg(A.rw + rid * (NW + 1) + w + 1);
   for (int it = b; it < e; ++it) {
     const int4 u = __ldg(A.units + it);
     const int J2 = u.y & 0xff, J1 = (u.y >> 8) & 0xff, cnt = u.y >> 16;
@@ -1029,16 +1040,17 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
       sred[((w * (T + 1) + m) * 2 + 1) * 8 + a] = ai[m];
     }
   }
-  __syncthreads();
+  yq_sync(g, NW * 32);
   constexpr int NH = c_half_off(T + 1);
   const int hb = c_half_off(J) + mb * (J + 1);
   const int fb = kQPad + c_full_off(J) + mb * (J + 1);
-  // stripes: warp w, lane group q -> output ma = w + kQWarps * q
-  const int ma = w + kQWarps * q;
+  // stripes: warp w, lane group q -> output ma = w + NW * q (NW * 4 >= 2J + 1)
+  static_assert(NW * 4 >= T + 1, "stripe coverage");
+  const int ma = w + NW * q;
   if (ma <= J) {
     double yr = 0.0, yi = 0.0;
     if (ma < L) {
-      for (int s = 0; s < kQWarps; ++s) {
+      for (int s = 0; s < NW; ++s) {
         yr += sred[((s * (T + 1) + ma) * 2 + 0) * 8 + a];
         yi += sred[((s * (T + 1) + ma) * 2 + 1) * 8 + a];
       }
@@ -1050,11 +1062,12 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
     reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
   }
   (void)NH;
-  __syncthreads();
+  yq_sync(g, NW * 32);
 }
 
-template <int T>
+template <int T, int GR>
 __global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs A) {
+  constexpr int NW = kQWarps / GR;
   constexpr int NF = c_full_off(T + 1);
   constexpr int NP = NF + 2 * kQPad;
   constexpr int NH = c_half_off(T + 1);
@@ -1084,18 +1097,21 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int a = lane & 7;
+  const int g = w / NW, wg = w - g * NW;
+  double* sredg = sred + (size_t)g * NW * (T + 1) * 2 * 8;
+  const int* rows = A.rows + (size_t)g * A.rows_cap;
   double* Yt = A.Y + (size_t)(atom0 + a) * NH * 2;
   double e_acc = 0.0;
   for (int q = 0;; ++q) {
-    const int code = __ldg(A.rows + q);
+    const int code = __ldg(rows + q);
     if (code < 0) break;
     const int j = code >> 6, mb = code & 63;
     const int rid = c_acc_off(j) + mb;
 #define YQROW(JJ)                                                                        \
   case JJ:                                                                               \
     if constexpr (JJ <= T) {                                                             \
-      if (2 * mb == JJ) yq_row<T, JJ, true>(sX, sred, lane, w, mb, rid, A, Yt, e_acc);   \
-      else yq_row<T, JJ, false>(sX, sred, lane, w, mb, rid, A, Yt, e_acc);               \
+      if (2 * mb == JJ) yq_row<T, JJ, true, GR>(sX, sredg, lane, g, wg, mb, rid, A, Yt, e_acc); \
+      else yq_row<T, JJ, false, GR>(sX, sredg, lane, g, wg, mb, rid, A, Yt, e_acc);          \
     }                                                                                    \
     break;
     switch (j) {

@@ -167,12 +167,19 @@ void launch_Y_t(snapgpu_ctx* c) {
       a.rw = c->d_qrw.p;
       a.cw = c->d_cw.p;
       a.rows = c->d_qrows.p;
+      a.rows_cap = c->yqplan.rows_cap;
       a.nlocal = c->nlocal;
       a.E = energy_out(c);
       const size_t smem = sizeof(double) * (2 * NP * 8 + (size_t)kQWarps * (T + 1) * 2 * 8);
-      CK(cudaFuncSetAttribute(k_compute_Y_quad<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
-      k_compute_Y_quad<T><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
+      if (c->yq_groups == 3) {
+        CK(cudaFuncSetAttribute(k_compute_Y_quad<T, 3>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_compute_Y_quad<T, 3><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
+      } else {
+        CK(cudaFuncSetAttribute(k_compute_Y_quad<T, 1>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_compute_Y_quad<T, 1><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
+      }
       CK(cudaGetLastError());
       return;
     }

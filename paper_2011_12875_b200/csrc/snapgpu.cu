@@ -438,7 +438,9 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     } else {
       if (c->y_impl == 3) {  // quad-unit tables (beta-independent part)
         up(c->d_expand, half_scatter_map(c->maps));
-        c->yqplan = yquad_plan(c->maps, kQWarps);
+        c->yq_groups = 3;  // 3 groups of 4 warps (A/B: SNAPGPU_YQ_GROUPS=1)
+        if (const char* e = std::getenv("SNAPGPU_YQ_GROUPS")) c->yq_groups = std::atoi(e) == 1 ? 1 : 3;
+        c->yqplan = yquad_plan(c->maps, kQWarps / c->yq_groups, c->yq_groups);
         std::vector<int4> u(c->yqplan.units.size());
         for (size_t q = 0; q < u.size(); ++q)
           u[q] = make_int4(c->yqplan.units[q][0], c->yqplan.units[q][1], c->yqplan.units[q][2],

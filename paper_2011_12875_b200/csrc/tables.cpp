@@ -384,7 +384,7 @@ YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps) {
   return p;
 }
 
-YQuadPlan yquad_plan(const IndexMaps& m, int warps) {
+YQuadPlan yquad_plan(const IndexMaps& m, int warps, int groups) {
   YQuadPlan p;
   std::vector<int> cwoff(m.tuples.size());
   int o = 0;
@@ -435,10 +435,13 @@ YQuadPlan yquad_plan(const IndexMaps& m, int warps) {
       }
       p.rw.push_back(off);
     }
-  std::stable_sort(rowcost.begin(), rowcost.end(),
-                   [](const auto& a, const auto& b) { return a.first > b.first; });
-  for (const auto& r : rowcost) p.rows.push_back(r.second);
-  p.rows.push_back(-1);
+  // rows LPT-split over the CTA's warp groups (decreasing cost per group)
+  std::vector<std::vector<int>> gb = lpt(rowcost, groups);
+  p.rows_cap = 1;
+  for (auto& b : gb) p.rows_cap = std::max<int>(p.rows_cap, static_cast<int>(b.size()) + 1);
+  p.rows.assign(static_cast<std::size_t>(groups) * p.rows_cap, -1);
+  for (int g = 0; g < groups; ++g)
+    for (std::size_t q = 0; q < gb[g].size(); ++q) p.rows[g * p.rows_cap + q] = gb[g][q];
   return p;
 }
 

@@ -114,9 +114,10 @@ struct YQuadPlan {
   std::vector<std::array<int, 4>> units;
   std::vector<std::array<int, 3>> items;
   std::vector<int> rw;
-  std::vector<int> rows;  // row codes j*64+mb (decreasing cost), -1 terminated
+  std::vector<int> rows;  // [group][rows_cap] row codes j*64+mb, -1 terminated
+  int rows_cap = 0;
 };
-YQuadPlan yquad_plan(const IndexMaps& m, int warps);
+YQuadPlan yquad_plan(const IndexMaps& m, int warps, int groups);
 std::vector<double> yquad_weights(const YQuadPlan& p, const IndexMaps& m,
                                   const std::vector<double>& wtab);
 
