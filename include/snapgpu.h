@@ -140,6 +140,13 @@ int snapgpu_set_positions(snapgpu_ctx* ctx, int natoms, const double* pos,
                           const double* box);
 int snapgpu_get_neighbors(snapgpu_ctx* ctx, int* numneigh, int* nbr, double* disp);
 
+/* Bispectrum descriptors B_l(i) (compute_B_from_U,
+ * snap_core.hpp:642-681) of the owned atoms, blist[i * ntriples + l], via the
+ * energy identity E_i = sum_l beta_l B_l(i) (compute_energy :684-701):
+ * compute_Y once per triple with one-hot beta (a fitting / validation path,
+ * ntriples compute_Y launches).  beta is restored; rerun the force step. */
+int snapgpu_compute_descriptors(snapgpu_ctx* ctx, double* blist);
+
 /* Virial of the owned pairs from dElist (the paper keeps
  * dElist for it): out6 = W_xx, W_yy, W_zz, W_xy, W_xz, W_yz
  * with W_ab = sum_{i,k} r_ik,a f_ik,b, r_ik the center -> neighbor

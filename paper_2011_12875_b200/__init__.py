@@ -89,6 +89,7 @@ def library() -> C.CDLL:
     L.snapgpu_get_ylist.argtypes = [vp, vp]
     L.snapgpu_get_dedr.argtypes = [vp, vp]
     L.snapgpu_get_virial.argtypes = [vp, vp]
+    L.snapgpu_compute_descriptors.argtypes = [vp, vp]
     L.snapgpu_set_positions.argtypes = [vp, ip, vp, vp]
     L.snapgpu_get_neighbors.argtypes = [vp, vp, vp, vp]
     L.snapgpu_device_outputs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
@@ -385,6 +386,13 @@ class SnapEngine:
         self._c(self._L.snapgpu_get_neighbors(self._h, nn.ctypes.data, nbr.ctypes.data,
                                               disp.ctypes.data))
         return nn, nbr, disp
+
+    def descriptors(self) -> np.ndarray:
+        """B_l(i), shape (nlocal, ntriples) (compute_B_from_U)."""
+        nt = counts(self.twojmax)["n_triples"]
+        o = np.zeros((self.nlocal, nt), np.float64)
+        self._c(self._L.snapgpu_compute_descriptors(self._h, o.ctypes.data))
+        return o
 
     def virial(self) -> np.ndarray:
         """W_xx, W_yy, W_zz, W_xy, W_xz, W_yz = sum_pairs r_ik (x) (-dE_ik)."""

@@ -523,6 +523,43 @@ int snapgpu_set_beta(snapgpu_ctx* c, const double* beta, int nbeta) {
   });
 }
 
+int snapgpu_compute_descriptors(snapgpu_ctx* c, double* blist) {
+  if (!c || !blist) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    need(c->have_lists, "compute_descriptors: no neighbor lists");
+    // B_l(i) through the energy identity E_i = sum_l beta_l B_l(i)
+    // (compute_energy, snap_core.hpp:684-701): compute_Y with one-hot beta
+    // per triple gives E_i = B_l(i) (compute_B_from_U, :642-681)
+    if (!c->have_U) launch_U(c);
+    const int nt = static_cast<int>(c->maps.triples.size());
+    const int n = c->nlocal;
+    const std::vector<double> saved = c->beta;
+    std::vector<double> col(std::max(1, n));
+    try {
+      for (int l = 0; l < nt; ++l) {
+        CK(cudaStreamSynchronize(c->stream));
+        c->beta.assign(nt, 0.0);
+        c->beta[l] = 1.0;
+        upload_beta(c);
+        launch_Y(c);
+        if (n > 0)
+          CK(cudaMemcpyAsync(col.data(), c->d_eatom.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                             c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i < n; ++i) blist[(size_t)i * nt + l] = col[i];
+      }
+    } catch (...) {
+      c->beta = saved;
+      upload_beta(c);
+      throw;
+    }
+    c->beta = saved;
+    upload_beta(c);
+    c->have_U = true;
+    c->have_Y = c->have_dE = false;  // Y' and the energies belong to the one-hot runs
+  });
+}
+
 int snapgpu_set_stream(snapgpu_ctx* c, void* s) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {

@@ -141,3 +141,38 @@ def test_device_neighbor_lists_bitwise_and_forces(snap, cells, jitter, seed):
         assert normerr(eng.forces(), ref.forces) <= 1e-13  # same lists; scatter order varies
         assert eng.energy()[1] == ref.etotal
     eng.close()
+
+
+def test_descriptors_vs_oracle_blist(snap, port):
+    """B_l(i) (compute_B_from_U, snap_core.hpp:642-681) from
+    one-hot-beta compute_Y runs equals the oracle's blist; the force step is
+    unchanged afterwards (beta restored)."""
+    from conftest import load_golden
+
+    for name in ("cluster_n6_2j8_s910_t1", "bcc54_2j8", "cluster_n5_2j4_s906_t1"):
+        p, out, _ = load_golden(name)
+        pr = snap.Problem.from_any(p)
+        eng = snap.SnapEngine.for_problem(pr)
+        eng.set_problem(pr)
+        b = eng.descriptors()
+        ref = port.run(pr, want=("blist",))["blist"]
+        assert normerr(b, ref) <= 1e-11, name
+        eng.run()
+        assert normerr(eng.forces(), out["forces"]) <= FTOL
+        eng.close()
+
+
+def test_report_row_schema_and_checksum(snap, port):
+    """a gpu row in the reference RunReport schema; the
+    checksum is the reference's (acceptance gate value on the oracle forces)."""
+    from paper_2011_12875_b200 import report
+
+    q = port.synthetic(64, 14, 8, seed=600)
+    assert report.checksum_hex(port.run(q, want=("forces",))["forces"]) == "dd6d6cc7a1c2e358"
+    p = snap.bcc_problem(4, 4, 4, twojmax=8)
+    row = report.gpu_row(p, steps=3)
+    csv = report.write_report_csv([row])
+    head = csv.splitlines()[0]
+    assert head.startswith(report.CSV_HEADER)
+    assert csv.splitlines()[1].startswith("gpu-b200,128,")
+    assert row["ok"] and row["katom_steps_per_s"] > 0 and len(row["force_checksum"]) == 16
