@@ -84,6 +84,7 @@ void plan_y(snapgpu_ctx* c) {
     // owns a whole tile, one 12-warp group (finest row granularity) when the
     // tile is split over several CTAs
     c->y_groups = (parts == 1) ? 3 : 1;
+    if (const char* e = std::getenv("SNAPGPU_Y_GROUPS")) c->y_groups = std::atoi(e) == 1 ? 1 : 3;
     std::vector<int> tasks =
         y_row_schedule(c->maps, c->ycplan[0].row_cost, parts * c->y_groups, &c->task_cap);
     c->d_tasks.alloc(tasks.size());
