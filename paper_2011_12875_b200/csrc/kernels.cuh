@@ -455,7 +455,7 @@ struct U2Cfg {
   static constexpr int WARPS = 4;
 };
 
-template <int T, int SL>
+template <int T, int SL, int PP>
 __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
     k_compute_U2(const UArgs A) {
   using C = U2Cfg<T, SL>;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
     nn = A.pr.numneigh[i];
     if (nn < 0 || nn > S) nn = 0;
   }
-  int passes = (nn + C::SL - 1) / C::SL;
+  int passes = (nn + C::SL * PP - 1) / (C::SL * PP);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) passes = max(passes, __shfl_xor_sync(0xffffffffu, passes, o));
 
@@ -533,64 +533,82 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
   for (int q = 0; q < NM; ++q) amr[q] = ami[q] = 0.0;
 
   for (int p = 0; p < passes; ++p) {
-    const int k = p * C::SL + s;
-    double ar = 1.0, ai = 0.0, br = 0.0, bi = 0.0, sf = 0.0;
-    if (k < nn) {
-      const double* g = geo + (size_t)(a * S + k) * 5;
-      ar = g[0];
-      ai = g[1];
-      br = g[2];
-      bi = g[3];
-      sf = g[4];
-    }
-    double vr[C::NC], vi[C::NC];
+    // PP pairs per lane per pass: independent recursions interleaved (ILP),
+    // summed into the same row accumulators
+    double ar[PP], ai[PP], br[PP], bi[PP], sf[PP];
 #pragma unroll
-    for (int c = 0; c < C::NC; ++c) vr[c] = vi[c] = 0.0;
-    vr[0] = (r == 0) ? 1.0 : 0.0;
-    accr[0] += sf * vr[0];
+    for (int pp = 0; pp < PP; ++pp) {
+      const int k = (p * PP + pp) * C::SL + s;
+      ar[pp] = 1.0;
+      ai[pp] = br[pp] = bi[pp] = sf[pp] = 0.0;
+      if (k < nn) {
+        const double* g = geo + (size_t)(a * S + k) * 5;
+        ar[pp] = g[0];
+        ai[pp] = g[1];
+        br[pp] = g[2];
+        bi[pp] = g[3];
+        sf[pp] = g[4];
+      }
+    }
+    double vr[PP][C::NC], vi[PP][C::NC];
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+#pragma unroll
+      for (int c = 0; c < C::NC; ++c) vr[pp][c] = vi[pp][c] = 0.0;
+      vr[pp][0] = (r == 0) ? 1.0 : 0.0;
+      accr[0] += sf[pp] * vr[pp][0];
+    }
 #pragma unroll
     for (int t = 1; t <= T; ++t) {
       if ((t & 1) == 0 && t < T + (T & 1)) {  // seed the new middle row t/2
         const bool creator = (2 * r == t);
         const double R = mirror_R(t);
 #pragma unroll
-        for (int c = 0; c < t; ++c) {
-          const double K = (((c + t / 2) & 1) ? -R : R);
-          const double sr = __shfl_up_sync(0xffffffffu, vr[t - 1 - c], 1);
-          const double si = __shfl_up_sync(0xffffffffu, vi[t - 1 - c], 1);
-          if (creator) {
-            vr[c] = K * sr;
-            vi[c] = -K * si;
+        for (int pp = 0; pp < PP; ++pp)
+#pragma unroll
+          for (int c = 0; c < t; ++c) {
+            const double K = (((c + t / 2) & 1) ? -R : R);
+            const double sr = __shfl_up_sync(0xffffffffu, vr[pp][t - 1 - c], 1);
+            const double si = __shfl_up_sync(0xffffffffu, vi[pp][t - 1 - c], 1);
+            if (creator) {
+              vr[pp][c] = K * sr;
+              vi[pp][c] = -K * si;
+            }
           }
-        }
       }
       if (t == T && (T & 1) == 0 && 2 * r + 2 == T) {  // transient last middle row
         const double R = mirror_R(T);
-        double plr = 0.0, pli = 0.0;
 #pragma unroll
-        for (int c = 0; c <= T / 2; ++c) {
-          const double K = (((c + T / 2) & 1) ? -R : R);
-          const double pr = K * vr[T - 1 - c], pi = -K * vi[T - 1 - c];
-          const double nr = ar * pr + ai * pi - br * plr - bi * pli;
-          const double ni = ar * pi - ai * pr - br * pli + bi * plr;
-          amr[c] = fma(sf, nr, amr[c]);
-          ami[c] = fma(sf, ni, ami[c]);
-          plr = pr;
-          pli = pi;
+        for (int pp = 0; pp < PP; ++pp) {
+          double plr = 0.0, pli = 0.0;
+#pragma unroll
+          for (int c = 0; c <= T / 2; ++c) {
+            const double K = (((c + T / 2) & 1) ? -R : R);
+            const double pr = K * vr[pp][T - 1 - c], pi = -K * vi[pp][T - 1 - c];
+            const double nr = ar[pp] * pr + ai[pp] * pi - br[pp] * plr - bi[pp] * pli;
+            const double ni = ar[pp] * pi - ai[pp] * pr - br[pp] * pli + bi[pp] * plr;
+            amr[c] = fma(sf[pp], nr, amr[c]);
+            ami[c] = fma(sf[pp], ni, ami[c]);
+            plr = pr;
+            pli = pi;
+          }
         }
       }
       // every lane advances its row (rows that do not exist yet are zero
       // and stay zero: no divergent branch)
 #pragma unroll
       for (int c = t; c >= 0; --c) {
-        const double pr = (c < t) ? vr[c] : 0.0, pi = (c < t) ? vi[c] : 0.0;
-        const double qr = (c > 0) ? vr[c - 1] : 0.0, qi = (c > 0) ? vi[c - 1] : 0.0;
-        const double nr = ar * pr + ai * pi - br * qr - bi * qi;
-        const double ni = ar * pi - ai * pr - br * qi + bi * qr;
-        vr[c] = nr;
-        vi[c] = ni;
-        accr[t * (t + 1) / 2 + c] = fma(sf, nr, accr[t * (t + 1) / 2 + c]);
-        acci[t * (t + 1) / 2 + c] = fma(sf, ni, acci[t * (t + 1) / 2 + c]);
+#pragma unroll
+        for (int pp = 0; pp < PP; ++pp) {
+          const double pr = (c < t) ? vr[pp][c] : 0.0, pi = (c < t) ? vi[pp][c] : 0.0;
+          const double qr = (c > 0) ? vr[pp][c - 1] : 0.0, qi = (c > 0) ? vi[pp][c - 1] : 0.0;
+          const double nr = ar[pp] * pr + ai[pp] * pi - br[pp] * qr - bi[pp] * qi;
+          const double ni = ar[pp] * pi - ai[pp] * pr - br[pp] * qi + bi[pp] * qr;
+          vr[pp][c] = nr;
+          vi[pp][c] = ni;
+          accr[t * (t + 1) / 2 + c] = fma(sf[pp], nr, accr[t * (t + 1) / 2 + c]);
+          acci[t * (t + 1) / 2 + c] = fma(sf[pp], ni, acci[t * (t + 1) / 2 + c]);
+        }
       }
     }
   }

@@ -5,6 +5,10 @@
 // context's twojmax to the instantiations below.
 #include "ctx.hpp"
 
+#ifndef SNAP_U2_PP
+#define SNAP_U2_PP 1  // pairs per lane per compute_U pass
+#endif
+
 #ifndef SNAP_T
 #error "compile with -DSNAP_T=<twojmax>"
 #endif
@@ -38,7 +42,7 @@ static L2Prefetch y_prefetch(snapgpu_ctx* c) {
   return P;
 }
 
-template <int T, int SL>
+template <int T, int SL, int PP = SNAP_U2_PP>
 static void launch_U2(snapgpu_ctx* c) {
   using C2 = U2Cfg<T, SL>;
   UArgs a;
@@ -47,11 +51,11 @@ static void launch_U2(snapgpu_ctx* c) {
   a.V = c->d_V.p;
   a.pf = y_prefetch<T>(c);
   const size_t smem = sizeof(double) * (size_t)C2::WARPS * C2::APW * c->stride * 5;
-  CK(cudaFuncSetAttribute(k_compute_U2<T, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(k_compute_U2<T, SL, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::max<size_t>(smem, 48 * 1024)));
   const int per_block = C2::WARPS * C2::APW;
   const int blocks = (c->nlocal + per_block - 1) / per_block;
-  k_compute_U2<T, SL><<<blocks, C2::WARPS * 32, smem, c->stream>>>(a);
+  k_compute_U2<T, SL, PP><<<blocks, C2::WARPS * 32, smem, c->stream>>>(a);
   CK(cudaGetLastError());
 }
 
