@@ -937,6 +937,9 @@ __global__ void __launch_bounds__(kYWinWarps * 32) k_compute_Y(const YArgs A) {
 // and their partial rows are combined by two xor-shuffles.  12 warps share
 // each target row (LPT over units), partial rows meet in shared memory.
 // ===========================================================================
+#ifndef SNAP_QU
+#define SNAP_QU 3  // window block length (2J=14: U = 2 / 3 -> 32.1 / 31.4 ms; 2J=12: U = 1 / 2 / 3 -> 7.07 / 6.56 / 6.43 ms)
+#endif
 constexpr int kQPad = 16;  // X pad: window reads reach J2+1 <= 15 below, D <= 14 above
 constexpr int kQWarps = 12;
 
@@ -972,7 +975,7 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
   constexpr int NP = NF + 2 * kQPad;
   constexpr int L = MID ? J / 2 + 1 : J + 1;
   constexpr int JW = J + 1;
-  constexpr int U = 2;
+  constexpr int U = SNAP_QU;
   const int q = lane >> 3, a = lane & 7;
   double ar[L], ai[L];
 #pragma unroll
