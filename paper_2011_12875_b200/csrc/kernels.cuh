@@ -1206,9 +1206,15 @@ __device__ __forceinline__ void group_sync(int g) {
 }
 constexpr int kYItemCap = 1024;  // row-pair units at 2J = 8: 838 (1479 items)
 #ifndef SNAP_Y_PAIR_U
-#define SNAP_Y_PAIR_U 2
+#define SNAP_Y_PAIR_U 1
 #endif
+// Window block lengths 1/1: the smallest code (122 KB vs 218 KB of SASS for
+// U = 2/3), which the cold-L2 step needs (bench: Y 104.2 -> 98.1 us at 2000
+// atoms; warm 92 us either way; 256k atoms 7.94 -> 7.66 ms).
 constexpr int kYPairU = SNAP_Y_PAIR_U;  // window block length of the paired loop
+#ifndef SNAP_Y_SINGLE_U
+#define SNAP_Y_SINGLE_U 1  // window block length of the single-item loop
+#endif
 
 // beta-independent tables of the constant-window kernel, in the constant bank
 // of the per-2J object (launch_t.cu, uploaded once per device): warp-uniform
@@ -1381,7 +1387,7 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
   const int* rb = (nw == 4 ? cYRowW4 : cYRowW12) + rid * (2 * nw + 1) + 2 * w;
   yw_units<2, kYPairU, L, JW, NP, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
-  yw_units<1, 3, L, JW, NP, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);        // singles
+  yw_units<1, SNAP_Y_SINGLE_U, L, JW, NP, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);        // singles
 #pragma unroll
   for (int m = 0; m < L; ++m) {
     sred[((w * (T + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
