@@ -1212,6 +1212,9 @@ constexpr int kYItemCap = 1024;  // row-pair units at 2J = 8: 838 (1479 items)
 // U = 2/3), which the cold-L2 step needs (bench: Y 104.2 -> 98.1 us at 2000
 // atoms; warm 92 us either way; 256k atoms 7.94 -> 7.66 ms).
 constexpr int kYPairU = SNAP_Y_PAIR_U;  // window block length of the paired loop
+// whole-tile CTAs (3 warp groups, large problems, warm code): block length 2
+// (262k atoms: 7.66 -> 7.56 ms)
+constexpr int kYPairU3 = 2;
 #ifndef SNAP_Y_SINGLE_U
 #define SNAP_Y_SINGLE_U 1  // window block length of the single-item loop
 #endif
@@ -1386,7 +1389,7 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
   const int* rb = (nw == 4 ? cYRowW4 : cYRowW12) + rid * (2 * nw + 1) + 2 * w;
-  yw_units<2, kYPairU, L, JW, NP, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
+  yw_units<2, (GR == 3 ? kYPairU3 : kYPairU), L, JW, NP, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
   yw_units<1, SNAP_Y_SINGLE_U, L, JW, NP, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);        // singles
 #pragma unroll
   for (int m = 0; m < L; ++m) {
