@@ -52,17 +52,25 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool own = true;  // false: a view into another buffer
   void alloc(size_t count) {
-    if (count <= n && p) return;
+    if (count <= n && p && own) return;
     release();
     if (count == 0) return;
     CK(cudaMalloc(&p, count * sizeof(T)));
     n = count;
   }
+  void view(T* ptr, size_t count) {
+    release();
+    p = ptr;
+    n = count;
+    own = false;
+  }
   void release() {
-    if (p) cudaFree(p);
+    if (p && own) cudaFree(p);
     p = nullptr;
     n = 0;
+    own = true;
   }
 };
 
@@ -109,11 +117,14 @@ struct snapgpu_ctx {
   snapgpu::host::DevBuf<int> d_numneigh, d_nbr, d_types;
   snapgpu::host::DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal, d_part;
   snapgpu::host::DevBuf<double> d_virial;  // virial partial sums + result
+  snapgpu::host::DevBuf<double> d_out;     // [forces | eatom | etotal]: one D2H per step
   snapgpu::host::DevBuf<double> d_nlpos;   // device neighbor-list build: positions, wrapped
   snapgpu::host::DevBuf<int> d_nlint;      // cell_of | members | counts | head | fill | max
   snapgpu::host::DevBuf<unsigned> d_ticket;
   snapgpu::host::DevBuf<unsigned> d_err;  // device validation flags (kErr*)
   unsigned* h_err = nullptr;              // pinned readback of d_err
+  double* h_out = nullptr;                // pinned staging of d_out (one-call API)
+  size_t h_out_n = 0;
 
   // graph
   cudaGraph_t graph = nullptr;

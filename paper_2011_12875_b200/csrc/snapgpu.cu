@@ -246,9 +246,16 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
     c->d_nbr.alloc(std::max<size_t>(1, nslots));
     c->d_disp.alloc(std::max<size_t>(1, nslots * 3));
     c->d_dedr.alloc(std::max<size_t>(1, nslots * 3));
-    c->d_forces.alloc((size_t)std::max(1, natoms_total) * 3);
-    c->d_eatom.alloc(std::max(1, nlocal));
-    c->d_etotal.alloc(1);
+    // forces, eatom and etotal are contiguous so the one-call API reads them
+    // back with a single copy
+    const size_t nf = (size_t)std::max(1, natoms_total) * 3, ne = std::max(1, nlocal);
+    c->d_forces.release();
+    c->d_eatom.release();
+    c->d_etotal.release();
+    c->d_out.alloc(nf + ne + 1);
+    c->d_forces.view(c->d_out.p, nf);
+    c->d_eatom.view(c->d_out.p + nf, ne);
+    c->d_etotal.view(c->d_out.p + nf + ne, 1);
     c->d_part.alloc((size_t)std::max(1, ntiles) * 4 * 8 + 64);  // >= Y grid size
     c->d_ticket.alloc(1);
     CK(cudaMemsetAsync(c->d_ticket.p, 0, sizeof(unsigned), c->stream));
@@ -503,6 +510,8 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_forces.release();
   c->d_eatom.release();
   c->d_etotal.release();
+  c->d_out.release();
+  if (c->h_out) cudaFreeHost(c->h_out);
   c->d_part.release();
   c->d_ticket.release();
   c->d_err.release();
@@ -669,16 +678,21 @@ int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, 
   return guarded(c, [&] {
     CK(cudaMemcpyAsync(c->h_err, c->d_err.p, sizeof(unsigned), cudaMemcpyDeviceToHost,
                        c->stream));
-    if (forces)
-      CK(cudaMemcpyAsync(forces, c->d_forces.p, sizeof(double) * 3 * c->natoms_total,
-                         cudaMemcpyDeviceToHost, c->stream));
-    if (eatom && c->nlocal > 0)
-      CK(cudaMemcpyAsync(eatom, c->d_eatom.p, sizeof(double) * c->nlocal, cudaMemcpyDeviceToHost,
-                         c->stream));
-    if (etotal)
-      CK(cudaMemcpyAsync(etotal, c->d_etotal.p, sizeof(double), cudaMemcpyDeviceToHost,
-                         c->stream));
+    // one D2H of [forces | eatom | etotal] into pinned staging, then host copies
+    const size_t nf = c->d_forces.n, ne = c->d_eatom.n, nout = nf + ne + 1;
+    if (c->h_out_n < nout) {
+      if (c->h_out) cudaFreeHost(c->h_out);
+      c->h_out = nullptr;
+      c->h_out_n = 0;
+      CK(cudaMallocHost(&c->h_out, nout * sizeof(double)));
+      c->h_out_n = nout;
+    }
+    CK(cudaMemcpyAsync(c->h_out, c->d_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (forces) std::memcpy(forces, c->h_out, sizeof(double) * 3 * c->natoms_total);
+    if (eatom && c->nlocal > 0) std::memcpy(eatom, c->h_out + nf, sizeof(double) * c->nlocal);
+    if (etotal) *etotal = c->h_out[nf + ne];
     if (*c->h_err) {
       const unsigned f = *c->h_err;
       CK(cudaMemsetAsync(c->d_err.p, 0, sizeof(unsigned), c->stream));
