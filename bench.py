@@ -2,37 +2,47 @@
 """Benchmark of the B200 SNAP force step (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2|C3|C4|C5]
 
-Workload (BASELINE.json configs[1], the metric's headline config): TestSNAP
-2J=8 tungsten, BCC a = 3.1803 A, 2000 atoms per GPU (10x10x10 cells per GPU,
-stacked along z for N GPUs: weak scaling), exactly 26 neighbors per atom,
-synthetic positions (seeded jitter) and random beta (no checkpoints exist).
+Workloads (BASELINE.json configs; TestSNAP tungsten BCC, a = 3.1803 A, seeded
+jitter, exactly 26 neighbors per atom, random beta, synthetic data):
+    C2 (default, the metric's headline config[1]): 2J=8, 2000 atoms per GPU
+        (10x10x10 cells per GPU, stacked along z for N GPUs: weak scaling)
+    C3: 2J=8, 262,144 atoms (64x64x32 cells), 1 B200 (saturation study)
+    C4: 2J=14, 32,768 atoms (32x32x16 cells), 1 B200 (high-J)
+    C5: 2J=8, 262,144 atoms per GPU (64x64x32 cells per GPU along z), weak
+        scaling with the NCCL force reduce-scatter
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under torch.distributed.run with N ranks (one per GPU, 127.0.0.1).
 
-A step is one full force evaluation through the reference stage order
+A step is one full force evaluation in the reference stage order
 (run_pipeline adjoint branch, pipeline.hpp:234-272): compute_U, compute_Y
-(+ per-atom energy), fused compute_dU/compute_deidrj, force scatter; with
-N > 1 also the NCCL force reduce-scatter and energy all-reduce.
+(+ per-atom energy), fused compute_dU/compute_deidrj, deterministic force
+scatter; with N > 1 also the one NCCL reduce-scatter that sums the partial
+forces and the energy.
 
 value    : whole-job Katom-steps/s (harness.hpp:443-447 grind definition),
            device-timed with CUDA events per step on the engine stream, L2
            flushed (256 MiB write) before every timed step, max over ranks.
-e2e      : the same metric through the public API with HOST buffers: every
-           step uploads that step's neighbor lists from pinned memory
-           (snapgpu_set_neighbors, incl. Problem::validate) and reads forces
-           and energies back (wall clock, synchronized).
+e2e      : the same metric through the public one-call API with HOST
+           buffers: every step uploads that step's neighbor lists from pinned
+           memory (deferred Problem::validate on the device, reverse-index
+           rebuild) and reads forces and energies back (wall clock, synced).
 roofline : FP64 SIMT (the CG contraction is sparse FP64; no tensor-core path):
-           algorithmic FLOPs of the dominant kernel (SURVEY.md §8(d) counts,
-           reference loop nests, mul and add counted separately) / its
+           algorithmic FLOPs of the dominant kernel (paper_2011_12875_b200.
+           flops, reference loop nests, mul and add counted separately) / its
            CUDA-event launch time, against the B200 FP64 spec peak.
 cpu_baseline : the unmodified reference (oracle/_ref/libsnapref.so, fused
            variant, deterministic, WorkerPool over all host threads) timed on
            this box on a bounded sample of the same workload (rank 0, N=1).
+--impl reference : the same reference alone, with this arm's metric/config.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -46,41 +56,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "grind time µs/atom-step (Katom-steps/s), 2J=8 W, vs FP64 roofline"
 FP64_SPEC_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: 148 SM x 64 DFMA/clk x 2 flop
-CELLS_PER_GPU = (10, 10, 10)
-
-
-# ---------------------------------------------------------------------------
-# algorithmic work (exact trip counts of the reference nests)
-# ---------------------------------------------------------------------------
-def flop_model(T: int) -> dict:
-    def zlb(j1, j2, j, mb, ma):
-        t = 2 * ma - j
-        ma1 = 0 if t + j1 - j2 < 0 else (t + j1 - j2) // 2
-        na = min(j1, (t + j2 + j1) // 2) - ma1 + 1
-        t = 2 * mb - j
-        mb1 = 0 if t + j1 - j2 < 0 else (t + j1 - j2) // 2
-        nb = min(j1, (t + j2 + j1) // 2) - mb1 + 1
-        return na, nb
-
-    mac = nb_sum = nz = 0
-    for j1 in range(T + 1):
-        for j2 in range(j1 + 1):
-            for j in range(j1 - j2, min(j1 + j2, T) + 1, 2):
-                for mb in range(j // 2 + 1):
-                    for ma in range(j + 1):
-                        na, nb = zlb(j1, j2, j, mb, ma)
-                        mac += na * nb
-                        nb_sum += nb
-                        nz += 1
-    nhalf = sum((t // 2 + 1) * (t + 1) for t in range(T + 1))
-    e_u = sum((t // 2 + 1) * t for t in range(1, T + 1))
-    e_c = 1 + sum((t + 1) * ((t + 1) // 2) + ((t // 2 + 1) if t % 2 == 0 else 0)
-                  for t in range(1, T + 1))
-    f_u = 18 * e_u + 4 * nhalf
-    f_y = 10 * mac + 4 * nb_sum + 4 * nz
-    f_de = 18 * e_u + 102 * e_u + 33 * e_c
-    return {"U_per_pair": f_u, "Y_per_atom": f_y, "dE_per_pair": f_de,
-            "per_atom_step_26": f_y + 26 * (f_u + f_de)}
+CONFIGS = {
+    "C2": {"cells": (10, 10, 10), "twojmax": 8,
+           "desc": "2J=8 tungsten, 2000 atoms/GPU (paper headline, BASELINE.json configs[1])"},
+    "C3": {"cells": (64, 64, 32), "twojmax": 8,
+           "desc": "2J=8 tungsten, 262144 atoms, 1 B200 (saturation, configs[2])"},
+    "C4": {"cells": (32, 32, 16), "twojmax": 14,
+           "desc": "2J=14 tungsten, 32768 atoms, 1 B200 (high-J, configs[3])"},
+    "C5": {"cells": (64, 64, 32), "twojmax": 8,
+           "desc": "2J=8 tungsten weak scaling, 262144 atoms/GPU (configs[4])"},
+}
 
 
 # ---------------------------------------------------------------------------
@@ -144,32 +129,109 @@ def dist_env():
     return ws, rank, local
 
 
-def build_problem(snap, ngpus: int, twojmax: int):
-    nx, ny, nz = CELLS_PER_GPU
-    return snap.bcc_problem(nx, ny, nz * ngpus, twojmax=twojmax)
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
-def cpu_reference_time(p, steps_cap=40, budget_s=12.0) -> dict:
-    """Time the unmodified reference (oracle/_ref) fused-det run_pipeline."""
+def workload_cells(cfg: str, n_gpus: int):
+    nx, ny, nz = CONFIGS[cfg]["cells"]
+    return nx, ny, nz * n_gpus
+
+
+def workload_config(args, n_gpus: int) -> dict:
+    """The `config` object of both arms (identical, so the driver can pair them)."""
+    c = CONFIGS[args.config]
+    nx, ny, nz = c["cells"]
+    per = 2 * nx * ny * nz
+    return {"workload": f"{args.config}: TestSNAP {c['desc']}; {per} atoms/GPU x 26 neighbors "
+                        f"({nx}x{ny}x{nz} BCC cells per GPU along z), {n_gpus} GPU(s)",
+            "config_id": args.config, "twojmax": c["twojmax"], "natoms_per_gpu": per,
+            "natoms_total": per * n_gpus, "neighbors_per_atom": 26,
+            "parallelism": f"atom-partition x{n_gpus}" + (
+                " + one NCCL reduce-scatter (forces + energy)" if n_gpus > 1 else ""),
+            "l2": "flushed by a 256 MiB write before every timed step"}
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N without a torchrun environment: run N ranks under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------------------
+# the reference (unmodified, oracle/_ref) on the host cores
+# ---------------------------------------------------------------------------
+def reference_problem(cells, T):
+    """The workload built with the oracle generators only (no product code):
+    BCC positions + beta (TestSNAP generator restated in oracle/snap_oracle.c)
+    and the reference's own neighbor builder (harness.hpp:119-202, cubic)."""
     import oracle
 
+    port = oracle.Port()
+    pos, beta, box = port.bcc(*cells, T)
+    if cells[0] == cells[1] == cells[2]:
+        numneigh, nbr, disp = oracle.Ref().neighborlist(pos, float(box[0]), 4.7)
+    else:  # the reference builder is cubic-only: its orthorhombic restatement
+        numneigh, nbr, disp = port.neighborlist(pos, box, 4.7)
+    from types import SimpleNamespace
+
+    return SimpleNamespace(twojmax=T, rcut=4.7, rmin0=0.0, rfac0=0.99363, wself=1.0,
+                           self_flag=1, beta=beta, weights=np.ones(1), types=None,
+                           numneigh=numneigh, nbr=nbr, disp=disp)
+
+
+def reference_sample_cells(cfg: str, n_gpus: int):
+    """Bounded sample of the workload for the CPU arm: the workload itself
+    when small, else a cubic lattice of the same material and band limit."""
+    cells = workload_cells(cfg, n_gpus)
+    natoms = 2 * cells[0] * cells[1] * cells[2]
+    T = CONFIGS[cfg]["twojmax"]
+    cap = 16000 if T <= 8 else 2000
+    if natoms <= cap:
+        return cells, ""
+    side = 20 if T <= 8 else 10
+    return (side, side, side), (f" (bounded sample: {2 * side ** 3} atoms of the same "
+                                f"workload; grind is per atom)")
+
+
+def cpu_reference_time(cfg: str, budget_s=12.0, steps_cap=40) -> dict:
+    """cpu_baseline of our arm: the reference fused-det force path."""
+    import oracle
+
+    cells, note = reference_sample_cells(cfg, 1)
+    T = CONFIGS[cfg]["twojmax"]
+    p = reference_problem(cells, T)
+    n = int(p.numneigh.shape[0])
     R = oracle.Ref()
     workers = os.cpu_count() or 1
-    ms, _, _ = R.time(p, "fused", True, workers, warmup=1, steps=1, with_energy=False)
+    ms, _, _ = R.time(p, "fused", True, workers, warmup=1, steps=1)
     steps = int(max(2, min(steps_cap, budget_s / max(ms[0] * 1e-3, 1e-3))))
-    ms, _, _ = R.time(p, "fused", True, workers, warmup=0, steps=steps, with_energy=False)
+    ms, _, _ = R.time(p, "fused", True, workers, warmup=0, steps=steps)
     secs = float(np.sum(ms)) * 1e-3
-    return {"value": p.natoms * steps / secs / 1000.0, "unit": "Katom-steps/s",
-            "cores": workers, "kind": "reference",
-            "sample": f"{p.natoms}-atom BCC W, 2J={p.twojmax}, reference run_pipeline "
-                      f"(fused, deterministic, force path) x {steps} steps after 1 warm-up, "
-                      f"WorkerPool({workers})",
+    return {"value": n * steps / secs / 1000.0, "unit": "Katom-steps/s",
+            "cores": workers, "kind": "reference", "cpu_model": cpu_model(),
+            "sample": f"{n}-atom BCC W, 2J={T}, reference run_pipeline (fused, "
+                      f"deterministic, force path; harness protocol: stage-time sum) x "
+                      f"{steps} steps after 1 warm-up, WorkerPool({workers}){note}",
             "ms_per_step": secs * 1e3 / steps}
 
 
-# ---------------------------------------------------------------------------
-# reference arm
-# ---------------------------------------------------------------------------
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -180,35 +242,41 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libsnapref.so not built (needs /root/reference)"}))
         return 0
-    import paper_2011_12875_b200 as snap  # problem generation only (host C++)
-
-    n_gpus = args.gpus
-    p = build_problem(snap, n_gpus, args.twojmax)
-    sample_note = ""
-    if p.natoms > 16000:  # bounded sample: same lattice, 16000 atoms
-        p = snap.bcc_problem(20, 20, 20, twojmax=args.twojmax)
-        sample_note = " (16000-atom sample of the workload; grind is per atom)"
+    n_gpus = max(ws, args.gpus)
+    cells, note = reference_sample_cells(args.config, n_gpus)
+    T = CONFIGS[args.config]["twojmax"]
+    p = reference_problem(cells, T)
+    n = int(p.numneigh.shape[0])
     R = oracle.Ref()
     workers = os.cpu_count() or 1
-    t_all = []
-    R.time(p, "fused", True, workers, warmup=min(args.warmup, 1), steps=1)
+    # harness protocol (harness.hpp:534-556): warm-up with energy, then the
+    # force path; W warm-ups like our arm
+    R.time(p, "fused", True, workers, warmup=args.warmup, steps=1)
+    t_all, w_all = [], []
     for _ in range(args.steps):
-        ms, _, _ = R.time(p, "fused", True, workers, warmup=0, steps=1, with_energy=False)
+        ms, wms, _, _ = R.time(p, "fused", True, workers, warmup=0, steps=1, wall=True)
         t_all.append(ms[0])
+        w_all.append(wms[0])
     secs = float(np.sum(t_all)) * 1e-3
-    value = p.natoms * len(t_all) / secs / 1000.0
+    value = n * len(t_all) / secs / 1000.0
+    # the oracle path (v1, deterministic): BASELINE.md §3
+    v1_steps = max(1, min(3, args.steps))
+    ms1, _, _ = R.time(p, "v1", True, workers, warmup=1, steps=v1_steps)
+    v1 = n * v1_steps / (float(np.sum(ms1)) * 1e-3) / 1000.0
     line = {
         "metric": METRIC, "value": value, "unit": "Katom-steps/s", "n_gpus": n_gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / len(t_all),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"TestSNAP 2J={args.twojmax} tungsten BCC, "
-                               f"{2000 * n_gpus} atoms x 26 neighbors{sample_note}",
-                   "twojmax": args.twojmax, "natoms_timed": p.natoms},
+        "config": workload_config(args, n_gpus),
         "cpu_baseline": {"value": value, "unit": "Katom-steps/s", "cores": workers,
-                         "kind": "reference",
-                         "sample": f"{p.natoms}-atom BCC, reference run_pipeline fused-det "
-                                   f"force path, {len(t_all)} steps, WorkerPool({workers})"},
+                         "kind": "reference", "cpu_model": cpu_model(),
+                         "sample": f"{n}-atom BCC W, 2J={T}, reference run_pipeline fused-det "
+                                   f"force path (harness protocol: stage-time sum), "
+                                   f"{len(t_all)} steps after {args.warmup} warm-ups, "
+                                   f"WorkerPool({workers}){note}",
+                         "wall_ms_per_step": float(np.mean(w_all)),
+                         "v1_det_katom_steps_s": v1},
         "e2e": {"value": value, "unit": "Katom-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -233,19 +301,18 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     import paper_2011_12875_b200 as snap
+    from paper_2011_12875_b200.distributed import PartitionedEngine
+    from paper_2011_12875_b200.flops import flop_model
 
     n_gpus = ws
-    T = args.twojmax
-    p = build_problem(snap, n_gpus, T)
+    T = CONFIGS[args.config]["twojmax"]
+    p = snap.bcc_problem(*workload_cells(args.config, n_gpus), twojmax=T)
     N = p.natoms
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    from paper_2011_12875_b200.distributed import PartitionedEngine
-
     pe = PartitionedEngine(p, n_gpus, rank, dev, stream)
     eng = pe.eng
     lo, hi = pe.lo, pe.hi
-    per = hi - lo
     own = pe.own
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -299,17 +366,17 @@ def run_ours(args):
     natoms_local = hi - lo
     stage_flops = {"U": fm["U_per_pair"] * npairs_local,
                    "Y": fm["Y_per_atom"] * natoms_local,
-                   "dE": fm["dE_per_pair"] * npairs_local, "forces": 6 * npairs_local}
+                   "dE": fm["dE_per_pair"] * npairs_local}
     dom = max(("U", "Y", "dE"), key=lambda k: stage_ms[k])
     achieved = stage_flops[dom] / (stage_ms[dom] * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{dom}_bytes_per_launch")
+            traffic = json.load(open(tpath)).get(args.config, {}).get(f"{dom}_bytes_per_launch")
         except Exception:
             traffic = None
-    step_flops = sum(v for k, v in stage_flops.items() if k != "forces")
+    step_flops = sum(stage_flops.values())
     whole_tflops = step_flops * n_gpus / (t_total * 1e-3 / args.steps) / 1e12
 
     # ---- end to end through the public API with host buffers ----------------
@@ -317,20 +384,24 @@ def run_ours(args):
     if not args.no_e2e:
         pin = [torch.from_numpy(a).pin_memory() for a in own]
         host_np = [t.numpy() for t in pin]
-        f_host = torch.zeros((N, 3), dtype=torch.float64).pin_memory()
-        e_host = torch.zeros(natoms_local, dtype=torch.float64).pin_memory().numpy()
-        t_host = torch.zeros(1, dtype=torch.float64).pin_memory().numpy()
+        if n_gpus == 1:
+            f_host = torch.zeros((N, 3), dtype=torch.float64).pin_memory().numpy()
+            e_host = torch.zeros(natoms_local, dtype=torch.float64).pin_memory().numpy()
+            t_host = torch.zeros(1, dtype=torch.float64).pin_memory().numpy()
+            d2h = f_host.nbytes + e_host.nbytes + 8
+        else:
+            c_host = torch.zeros(pe.chunk.numel(), dtype=torch.float64).pin_memory()
+            d2h = c_host.numel() * 8
         h2d = sum(a.nbytes for a in host_np)
-        d2h = (pe.f_own.numel() if n_gpus > 1 else N * 3) * 8 + natoms_local * 8 + 8
 
         def e2e_step():
             if n_gpus == 1:  # the public one-call API: upload, run, read back
-                eng.step(*host_np, forces=f_host.numpy(), eatom=e_host, etotal=t_host)
-            else:
+                eng.step(*host_np, forces=f_host, eatom=e_host, etotal=t_host)
+            else:  # upload the owned lists, step (+ reduce-scatter), read the chunk
                 pe.upload(*host_np)
-                step()
-                f_host.view(-1)[: pe.f_own.numel()].copy_(pe.f_own, non_blocking=False)
-                eng.energy()
+                pe.step()
+                c_host.copy_(pe.chunk, non_blocking=True)
+                stream.synchronize()
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
@@ -361,7 +432,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_time(p)
+            cpu = cpu_reference_time(args.config)
         except Exception as e:  # oracle/_ref absent on this box
             cpu = {"value": None, "unavailable": str(e)[:200]}
 
@@ -372,14 +443,7 @@ def run_ours(args):
             "ms_per_step": t_total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "grind_us_per_atom_step": 1000.0 / value,
-            "config": {"workload": f"TestSNAP 2J={T} tungsten BCC, {per} atoms/GPU x 26 "
-                                   f"neighbors (10x10x{10 * n_gpus} cells)",
-                       "twojmax": T, "natoms_per_gpu": per, "natoms_total": N,
-                       "neighbors_per_atom": 26,
-                       "parallelism": f"atom-partition x{n_gpus}" + (
-                           " + NCCL reduce-scatter(forces) + all-reduce(energy)"
-                           if n_gpus > 1 else ""),
-                       "l2": "flushed by a 256 MiB write before every timed step"},
+            "config": workload_config(args, n_gpus),
             "stages_ms": stage_ms,
             "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved,
                          "peak": FP64_SPEC_TFLOPS, "unit": "TFLOP/s",
@@ -393,8 +457,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            # our kernels per step: U, Y (+energy), fused dU/dE (+scatter when fused)
-            "gpu_launches": (3 if per * p.stride <= (1 << 18) else 4) * args.steps,
+            # our kernels per timed step: U, Y (+energy), fused dU/dE, force gather
+            "gpu_launches": 4 * args.steps,
             "reference_points": {"v100_kokkos_baseline_katom_steps_s": 32.8,
                                  "v100_final_lammps_derived_katom_steps_s": 643},
         }
@@ -405,21 +469,34 @@ def run_ours(args):
     return 0
 
 
+def run_dry(args):
+    """Launch check without a GPU: each rank reports its place in the job."""
+    ws, rank, local = dist_env()
+    print(json.dumps({"dry_run": True, "rank": rank, "world": ws, "local_rank": local,
+                      "config": workload_config(args, max(ws, 1))}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--twojmax", type=int, default=8)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, _, _ = dist_env()
-    if ws > 1 and args.gpus != ws:
+    if ws == 1 and args.gpus > 1 and "LOCAL_RANK" not in os.environ:
+        return relaunch_distributed(args)
+    if ws > 1:
         args.gpus = ws
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

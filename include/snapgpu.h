@@ -98,7 +98,12 @@ int snapgpu_compute_Y(snapgpu_ctx* ctx);         /* compute_Y        :1085,
 int snapgpu_compute_dU_deidrj(snapgpu_ctx* ctx); /* compute_fused_dE :1274
                                                     (compute_dU :707 fused
                                                     with compute_dE :1206)  */
-int snapgpu_scatter_forces(snapgpu_ctx* ctx);    /* scatter_forces   :872  */
+int snapgpu_scatter_forces(snapgpu_ctx* ctx);    /* scatter_forces   :872,
+                                                    deterministic mode
+                                                    (:889-899): each force is
+                                                    the serialized pair-order
+                                                    sum of dElist, bitwise
+                                                    reproducible run to run */
 
 /* The whole force step in reference stage order (run_pipeline adjoint
  * branch, pipeline.hpp:234-272): U -> Y(+energy) -> fused dU/dE -> scatter.
@@ -117,7 +122,8 @@ int snapgpu_run_host(snapgpu_ctx* ctx, int natoms_total, int atom_lo, int nlocal
                      double* eatom, double* etotal);
 
 /* ---- results (host copies; synchronize the stream) ---------------------
- * forces: natoms_total x 3 (PipelineResult::forces, pipeline.hpp:50);
+ * forces: natoms_total x 3 (PipelineResult::forces, pipeline.hpp:50), or
+ * the chunked layout of snapgpu_set_force_layout;
  * eatom: nlocal (EnergyReport::per_atom); etotal: sum over owned atoms. */
 int snapgpu_get_forces(snapgpu_ctx* ctx, double* forces);
 int snapgpu_get_energy(snapgpu_ctx* ctx, double* eatom, double* etotal);
@@ -156,7 +162,7 @@ int snapgpu_compute_descriptors(snapgpu_ctx* ctx, double* blist);
 int snapgpu_get_virial(snapgpu_ctx* ctx, double* out6);
 
 /* Device pointers for collectives (valid until the next set_neighbors):
- * forces natoms_total x 3, eatom nlocal, etotal 1. */
+ * forces (natoms_total x 3, or the chunked layout), eatom nlocal, etotal 1. */
 int snapgpu_device_outputs(snapgpu_ctx* ctx, double** forces, double** eatom,
                            double** etotal);
 
@@ -173,9 +179,21 @@ int snapgpu_get_energy_device(snapgpu_ctx* ctx, double* eatom_dst,
 int snapgpu_enable_stage_timing(snapgpu_ctx* ctx, int on);
 int snapgpu_stage_times(snapgpu_ctx* ctx, float* out4);
 
-/* compute_Y launch knobs (benchmark sweeps); 0 = automatic: warps per CTA
- * (<= 8), row-list parts per tile, atoms per CTA tile (8, 16 or 32). */
-int snapgpu_tune(snapgpu_ctx* ctx, int y_warps, int y_parts, int y_tile_atoms);
+/* compute_Y launch knob (benchmark sweeps, 2J <= 8): CTAs per 32-atom tile
+ * splitting its target rows, in [1, 8]; 0 = automatic (fill the SMs). */
+int snapgpu_tune(snapgpu_ctx* ctx, int y_parts);
+
+/* Force output layout for the atom-partitioned multi-GPU step
+ * (the coupling is scatter_forces snap_core.hpp:889-898 and
+ * the energy sum :692-699).  nchunks = world size: atom a's force lands at
+ * (a / k) * (3k + 1) + (a % k) * 3 with k = ceil(natoms_total / nchunks), and
+ * slot r * (3k + 1) + 3k of every chunk r receives this context's total
+ * energy, so ONE reduce-scatter (sum, chunk 3k + 1 doubles) hands rank r its
+ * owned forces and the total energy.  ext_forces: caller-owned device buffer
+ * of nchunks * (3k + 1) doubles that the force gather writes into (NULL: the
+ * context's own buffer).  nchunks = 1 restores the plain natoms x 3 array.
+ * Takes effect at the next neighbor-list upload. */
+int snapgpu_set_force_layout(snapgpu_ctx* ctx, int nchunks, double* ext_forces);
 
 /* ---- context-free host utilities --------------------------------------- */
 

@@ -248,7 +248,8 @@ class Ref:
         L.ref_last_error.restype = C.c_char_p
         L.ref_run.argtypes = self._PROB + [C.c_char_p, C.c_int, C.c_int] + [C.c_void_p] * 7
         L.ref_time.argtypes = self._PROB + [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int,
-                                            C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+                                            C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]
         L.ref_build_neighborlist.argtypes = [_dp, C.c_int, C.c_double, C.c_double, C.c_int,
                                              C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_cg_table.argtypes = [C.c_int, _dp]
@@ -316,16 +317,23 @@ class Ref:
         return res
 
     def time(self, p, variant="fused", deterministic=True, workers=1, warmup=1, steps=5,
-             with_energy=False):
+             with_energy=False, wall=False):
+        """Per-step times (ms) of run_pipeline in the harness protocol
+        (harness.hpp:534-556): PipelineResult::total_ms, the stage-time sum;
+        with wall=True also the wall clock around each call."""
         d = _arrays(p)
         ms = np.zeros(steps, np.float64)
+        wms = np.zeros(steps, np.float64)
         forces = np.zeros((d.natoms, 3), np.float64)
         et = np.zeros(1, np.float64)
         rc = self.L.ref_time(*self._pargs(p, d), variant.encode(), int(deterministic),
                              int(workers), int(warmup), int(steps), int(with_energy),
-                             ms.ctypes.data, forces.ctypes.data, et.ctypes.data)
+                             ms.ctypes.data, wms.ctypes.data, forces.ctypes.data,
+                             et.ctypes.data)
         if rc:
             raise ValueError(self.err())
+        if wall:
+            return ms, wms, forces, float(et[0])
         return ms, forces, float(et[0])
 
     def neighborlist(self, pos, box, rcut):

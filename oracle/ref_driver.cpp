@@ -164,14 +164,18 @@ int ref_run(int twojmax, double rcut, double rmin0, double rfac0, double wself,
 // run_pipeline timing (pipeline.hpp:206): `warmup` full evaluations (with
 // energy), then `steps` force-path evaluations (with_energy = false), the
 // harness protocol of harness.hpp:534-556.  step_ms[steps] receives each
-// step's wall time.
+// step's PipelineResult::total_ms, the sum of its stage times (what the
+// harness reports, harness.hpp:540-545: the per-call Problem::validate,
+// index-map and CG-table setup of run_pipeline, pipeline.hpp:211-216, are
+// not part of a step); wall_ms[steps] (may be NULL) the wall clock around
+// the whole call.
 int ref_time(int twojmax, double rcut, double rmin0, double rfac0, double wself,
              int self_flag, const double* beta, int nbeta,
              const double* weights, int nweights, int natoms, int stride,
              const int* numneigh, const int* nbr, const double* disp,
              const int* types, const char* variant_name, int deterministic,
              int workers, int warmup, int steps, int with_energy,
-             double* step_ms, double* forces, double* etotal) {
+             double* step_ms, double* wall_ms, double* forces, double* etotal) {
   return guarded([&] {
     Problem p = make_problem(twojmax, rcut, rmin0, rfac0, wself, self_flag, beta,
                              nbeta, weights, nweights, natoms, stride, numneigh,
@@ -187,7 +191,8 @@ int ref_time(int twojmax, double rcut, double rmin0, double rfac0, double wself,
       const auto t0 = std::chrono::steady_clock::now();
       PipelineResult r = run_pipeline(p, v, mode, pool, 0, with_energy != 0);
       const auto t1 = std::chrono::steady_clock::now();
-      step_ms[s] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+      step_ms[s] = r.total_ms;
+      if (wall_ms) wall_ms[s] = std::chrono::duration<double, std::milli>(t1 - t0).count();
       if (forces && s == steps - 1) std::copy(r.forces.begin(), r.forces.end(), forces);
       if (etotal && with_energy) *etotal = r.energy.total;
     }

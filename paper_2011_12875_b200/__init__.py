@@ -34,7 +34,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SNAPGPU_LIB") or os.path.join(_HERE, "_build", "libsnapgpu.so")  # env: A/B builds (development)
+LIB_PATH = os.path.join(_HERE, "_build", "libsnapgpu.so")
 
 
 class InvalidArgument(ValueError):
@@ -98,7 +98,8 @@ def library() -> C.CDLL:
     L.snapgpu_fp64_peak.argtypes = [ip, ip, vp, vp]
     L.snapgpu_enable_stage_timing.argtypes = [vp, ip]
     L.snapgpu_stage_times.argtypes = [vp, vp]
-    L.snapgpu_tune.argtypes = [vp, ip, ip, ip]
+    L.snapgpu_tune.argtypes = [vp, ip]
+    L.snapgpu_set_force_layout.argtypes = [vp, ip, vp]
     L.snapgpu_counts.argtypes = [ip, vp]
     L.snapgpu_build_neighborlist.argtypes = [vp, ip, vp, dp, ip, vp, vp, vp]
     L.snapgpu_bcc_lattice.argtypes = [ip, ip, ip, dp, dp, C.c_uint64, ip, vp, vp]
@@ -328,9 +329,17 @@ class SnapEngine:
     def synchronize(self):
         self._c(self._L.snapgpu_synchronize(self._h))
 
-    def tune(self, y_warps=0, y_parts=0, y_tile_atoms=0):
-        """compute_Y launch knobs (0 = automatic)."""
-        self._c(self._L.snapgpu_tune(self._h, int(y_warps), int(y_parts), int(y_tile_atoms)))
+    def tune(self, y_parts=0):
+        """compute_Y CTAs per 32-atom tile, 1..8 (0 = automatic)."""
+        self._c(self._L.snapgpu_tune(self._h, int(y_parts)))
+
+    def set_force_layout(self, nchunks=1, ext_forces_ptr=None):
+        """Chunked force output for the partitioned multi-GPU step
+        (snapgpu_set_force_layout): one chunk of ceil(natoms/nchunks) atoms
+        plus an energy slot per rank, optionally written straight into a
+        caller-owned device buffer.  Takes effect at the next list upload."""
+        self._c(self._L.snapgpu_set_force_layout(self._h, int(nchunks), ext_forces_ptr))
+        self._nchunks = int(nchunks)
 
     def enable_stage_timing(self, on=True):
         self._c(self._L.snapgpu_enable_stage_timing(self._h, int(bool(on))))
@@ -342,7 +351,13 @@ class SnapEngine:
 
     # -- outputs -------------------------------------------------------------
     def forces(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        f = out if out is not None else np.zeros((self.natoms_total, 3), np.float64)
+        """natoms_total x 3 forces (with a chunked layout: the raw chunks)."""
+        nch = getattr(self, "_nchunks", 1)
+        if nch > 1:
+            k = -(-self.natoms_total // nch)
+            f = out if out is not None else np.zeros(nch * (3 * k + 1), np.float64)
+        else:
+            f = out if out is not None else np.zeros((self.natoms_total, 3), np.float64)
         self._c(self._L.snapgpu_get_forces(self._h, f.ctypes.data))
         return f
 

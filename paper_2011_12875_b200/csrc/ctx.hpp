@@ -91,47 +91,57 @@ struct snapgpu_ctx {
   std::vector<double> cg, hf, ywgt;
 
   // device tables
-  snapgpu::host::DevBuf<double> d_weights, d_itw, d_cw, d_citw[2];
-  snapgpu::host::DevBuf<int4> d_items;
-  snapgpu::host::DevBuf<int> d_rowbeg, d_tasks, d_expand;
+  snapgpu::host::DevBuf<double> d_weights, d_cw, d_citw[2];
+  snapgpu::host::DevBuf<int> d_tasks, d_expand;
   snapgpu::YPlan yplan;
   snapgpu::YCoopPlan ycplan[2];  // constant-window units for 4 / 12 warps per row
   snapgpu::YQuadPlan yqplan;     // quad units (2J > 8)
-  int yq_groups = 3;             // warp groups per quad-unit CTA (1 or 3)
   snapgpu::host::DevBuf<int4> d_qunits;
   snapgpu::host::DevBuf<double> d_qitw;
   snapgpu::host::DevBuf<int> d_qrw, d_qrows;
-  int y_impl = 0;  // 0: constant-window (2J <= 8), 3: quad units (2J > 8), 2: half-V window
-  int de_impl = 0;  // 0: reverse-mode fused dE, 1: forward-mode (three du stacks)
-  int u_impl = 0;   // 0: row-lane compute_U (2J <= 8), 1: column-lane compute_U
   int task_cap = 0;
-  int y_warps = 8, y_parts = 0, y_parts_used = 1, de_warps = 0;  // y_warps set in create
-  int y_ta = 32, y_ta_max = 32, y_ta_req = 0;
+  int y_parts = 0, y_parts_used = 1;  // compute_Y CTAs per 32-atom tile (0 = automatic)
   int y_groups = 3;  // warp groups per constant-window compute_Y CTA (1 or 3)
 
   // problem shape
   int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
-  bool have_lists = false, have_U = false, have_Y = false, have_dE = false;
+  bool have_lists = false, have_U = false, have_Y = false, have_dE = false, have_forces = false;
 
   // device arrays
   snapgpu::host::DevBuf<int> d_numneigh, d_nbr, d_types;
-  snapgpu::host::DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal, d_part;
+  snapgpu::host::DevBuf<double> d_disp, d_V, d_Y, d_dedr, d_forces, d_eatom, d_etotal;
   snapgpu::host::DevBuf<double> d_virial;  // virial partial sums + result
   snapgpu::host::DevBuf<double> d_out;     // [forces | eatom | etotal]: one D2H per step
   snapgpu::host::DevBuf<double> d_nlpos;   // device neighbor-list build: positions, wrapped
   snapgpu::host::DevBuf<int> d_nlint;      // cell_of | members | counts | head | fill | max
-  snapgpu::host::DevBuf<unsigned> d_ticket;
-  snapgpu::host::DevBuf<unsigned> d_err;  // device validation flags (kErr*)
-  unsigned* h_err = nullptr;              // pinned readback of d_err
-  double* h_out = nullptr;                // pinned staging of d_out (one-call API)
+  snapgpu::host::DevBuf<unsigned> d_err;   // device validation flags (kErr*)
+  unsigned* h_err = nullptr;               // pinned readback of d_err
+  double* h_out = nullptr;                 // pinned staging of d_out (one-call API)
   size_t h_out_n = 0;
 
-  // graph
+  // deterministic energy epilogue (kernels.cuh energy_epilogue)
+  snapgpu::host::DevBuf<double> d_epart, d_tile_sum;
+  snapgpu::host::DevBuf<unsigned> d_tickets;  // [0]: global ticket, [1..]: per tile
+
+  // deterministic force gather (kernels.cuh k_gather_forces): reverse
+  // neighbor index, rebuilt when the lists change
+  snapgpu::host::DevBuf<int> d_rev_off, d_rev_cur, d_rev;
+  bool csr_dirty = true;
+  // force output layout: nchunks chunks of chunk_rows atoms (+ energy slot
+  // when nchunks > 1), into the caller's device buffer when ext_forces is set
+  int nchunks = 1;
+  double* ext_forces = nullptr;
+  int chunk_rows() const {
+    return nchunks > 1 ? (natoms_total + nchunks - 1) / nchunks : (natoms_total > 0 ? natoms_total : 1);
+  }
+  int chunk_stride() const { return nchunks > 1 ? 3 * chunk_rows() + 1 : 3 * chunk_rows(); }
+
+  // graphs: the force step, and the reverse-index build
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   bool graph_valid = false;
-
-  bool fuse_scatter = true;  // dE kernel scatters forces (reference `fused` variant)
+  cudaGraph_t csr_graph = nullptr;
+  cudaGraphExec_t csr_gexec = nullptr;
 
   // timing
   bool timing = false;
@@ -162,8 +172,10 @@ inline PairArgs pair_args(const snapgpu_ctx* c) {
 inline EnergyOut energy_out(snapgpu_ctx* c) {
   EnergyOut E;
   E.eatom = c->d_eatom.p;
-  E.part_sums = c->d_part.p;
-  E.ticket = c->d_ticket.p;
+  E.epart = c->d_epart.p;
+  E.tile_sum = c->d_tile_sum.p;
+  E.ticket = c->d_tickets.p;
+  E.tile_ticket = c->d_tickets.p + 1;
   E.etotal = c->d_etotal.p;
   return E;
 }

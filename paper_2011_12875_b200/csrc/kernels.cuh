@@ -1,14 +1,14 @@
 // kernels.cuh -- sm_100a FP64 kernels of the B200 SNAP force step.
 //
 // Stage map (reference: /root/reference/proj/include/snapforge/snap_core.hpp):
-//   k_compute_U        compute_U            :369-489   (fused with the 3-sphere
-//                                                        map + switching function)
-//   k_compute_Y        compute_Y            :1085-1200  (sliding-window CG
-//                                                        contraction, any twojmax)
-//                      + per-atom energy (replaces compute_B_from_U :642 and
-//                        compute_energy :684 through E_i = 1/3 sum Y:U*)
-//   k_fused_dE         compute_fused_dE     :1274-1406 (dU never reaches HBM)
-//   k_scatter_forces   scatter_forces       :872-953
+//   k_compute_U2 / k_compute_U  compute_U         :369-489   (fused with the
+//                                                  3-sphere map + switching function)
+//   k_compute_Y_cwin (2J<=8)    compute_Y         :1085-1200 (CG contraction)
+//   k_compute_Y_quad (2J>8)       + per-atom energy (replaces compute_B_from_U
+//                                   :642 and compute_energy :684 through
+//                                   E_i = 1/3 sum Y:U*)
+//   k_fused_dE_rev              compute_fused_dE  :1274-1406 (dU never exists)
+//   k_gather_forces             scatter_forces    :872-953   (deterministic pull)
 //
 // All arithmetic is FP64 on the SIMT pipe (the CG contraction is sparse;
 // no tensor-core path exists for it).  Every kernel works in "v-space"
@@ -24,7 +24,7 @@
 //   Y' (ylist, v-space, weighted) [atom][half idx][re,im]  (atom-major: the
 //                                  fused dE kernel reads one atom per pair)
 //   dedr                          [atom][slot][3]
-//   forces                        [atom][3]
+//   forces                        [atom][3] (one chunk per rank when partitioned)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -665,264 +665,60 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
 }
 
 // ---------------------------------------------------------------------------
-// Energy epilogue shared by the compute_Y kernels: per-atom energies are
-// accumulated into eatom (atomics; one add per CTA that touched the atom), the
-// CTA's partial total goes to part_sums[block], and the last CTA to finish
-// (threadfence + ticket) sums part_sums in block order into *etotal, so the
-// total is deterministic and needs no extra launch.
+// Energy epilogue shared by the compute_Y kernels (replaces compute_energy,
+// snap_core.hpp:684-701), deterministic whatever the launch split: a tile of
+// APT atoms may be spread over `parts` CTAs (grid.y).  Each CTA stores its
+// lane energies in its own slot; the tile's last CTA (ticket) sums the parts
+// in part order into eatom and the tile's energy into tile_sum; the last
+// tile sums tile_sum in tile order into *etotal.  No extra launch, and the
+// result does not depend on which CTA finishes first.
 // ---------------------------------------------------------------------------
 struct EnergyOut {
-  double* eatom;
-  double* part_sums;   // one per CTA
-  unsigned* ticket;    // zero at launch; reset by the last CTA
+  double* eatom;          // [nlocal]
+  double* epart;          // [parts][ntiles][APT] per-CTA lane energies
+  double* tile_sum;       // [ntiles]
+  unsigned* tile_ticket;  // [ntiles], zero at launch; reset by each tile's last CTA
+  unsigned* ticket;       // zero at launch; reset by the last tile
   double* etotal;
 };
 
+template <int APT>
 __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_e, bool valid,
                                                 int atom) {
-  // called by one full warp of the CTA
+  // called by one full warp of the CTA; lanes >= APT carry no atom
   const int lane = threadIdx.x & 31;
-  if (valid) atomicAdd(E.eatom + atom, lane_e);
-  double s = valid ? lane_e : 0.0;
+  const unsigned tile = blockIdx.x, ntiles = gridDim.x, parts = gridDim.y;
+  if (lane < APT) E.epart[((size_t)blockIdx.y * ntiles + tile) * APT + lane] = valid ? lane_e : 0.0;
+  __threadfence();
+  __syncwarp();
+  unsigned t = 0;
+  if (lane == 0) t = atomicAdd(E.tile_ticket + tile, 1u);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t != parts - 1) return;
+  __threadfence();  // this CTA saw every part of its tile
+  double e = 0.0;
+  if (lane < APT)
+    for (unsigned q = 0; q < parts; ++q) e += __ldcg(E.epart + ((size_t)q * ntiles + tile) * APT + lane);
+  if (valid) E.eatom[atom] = e;
+  double s = valid ? e : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const unsigned nblk = gridDim.x * gridDim.y;
-  const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
-  unsigned t = 0;
   if (lane == 0) {
-    E.part_sums[bid] = s;
+    E.tile_sum[tile] = s;
+    E.tile_ticket[tile] = 0u;
     __threadfence();
     t = atomicAdd(E.ticket, 1u);
   }
   t = __shfl_sync(0xffffffffu, t, 0);
-  if (t == nblk - 1) {  // last CTA: deterministic ordered sum
-    __threadfence();
-    double acc = 0.0;
-    for (unsigned b = lane; b < nblk; b += 32) acc += __ldcg(E.part_sums + b);
+  if (t != ntiles - 1) return;
+  __threadfence();  // last tile: ordered sum of the tile energies
+  double acc = 0.0;
+  for (unsigned b = lane; b < ntiles; b += 32) acc += __ldcg(E.tile_sum + b);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      *E.etotal = acc;
-      *E.ticket = 0u;
-    }
-  }
-}
-
-// ===========================================================================
-// compute_Y  (snap_core.hpp:1085-1200), any twojmax <= 14
-//
-// Lanes = atoms of an AoSoA tile (every lane runs the same loop bounds and
-// reads the same coefficient), TA = 32 atoms per CTA when the half-storage V
-// tile fits in shared memory (2J <= 10), else 16 atoms with the two
-// half-warps splitting the a2 loop.  Each warp owns whole target rows (j, mb)
-// and keeps the row's outputs in registers across every contributing "row
-// pair" item (coupling tuple (j1, j2) -> j, factor rows mb1 of level j1 and
-// mb2 = mb + D - mb1 of level j2, D = (j1+j2-j)/2).  Per item the kernel runs
-// a runtime loop over the elements a2 of the shorter factor row and keeps a
-// sliding register window of the longer row aligned with the outputs:
-//     acc[ma] += C'(a1 = ma + D - a2, a2) * x1[a1] * (w * x2[a2])
-// so each step loads one new x1 element and one x2 element for j+1 complex
-// MACs; the window length j+1 (j/2+1 on the middle row, whose upper half is
-// never read) is a template parameter, so the whole kernel is a handful of
-// small loops (no instruction-cache pressure) while all arithmetic operands
-// stay in registers.  Coefficients C' (v-space CG, zero-padded per a2 row)
-// and the per-item W' factors are host-built (tables.cpp).
-// Output: Y' (v-space, weighted); epilogue E_i = 2/3 sum Re(Y'_s conj V).
-// ===========================================================================
-struct YArgs {
-  const double* V;        // [tile32][2][NH][32]
-  double* Y;              // [tile32][2][NH][32]
-  const int4* items;      // row-pair items: x1 row base, x2 row base, packed dims, coef off
-  const double* itw;      // W' per item
-  const int* row_begin;   // per target row id (j,mb): item range [begin, end)
-  const double* cw;       // windowed C' table
-  const int* tasks;       // [worker][cap] row codes j*64+mb, -1 terminated
-  int task_cap;
-  int nlocal;
-  EnergyOut E;
-};
-
-__device__ __forceinline__ double flip_sign(double x, unsigned mask) {
-  return __hiloint2double(__double2hiint(x) ^ (int)mask, __double2loint(x));
-}
-
-// Element a of factor row X(t, mb, .) from the half-storage tile: stored rows
-// directly, mirrored rows (2 mb > t) through u(t-mb,t-ma) = (-1)^(ma+mb) conj u(mb,ma)
-// (halfint_index.hpp:22-25); the (-1)^mb factor is folded into W'.
-struct RowRef {
-  const double* p;  // re plane element 0 of the row walk (lane offset applied)
-  int step;         // +TA or -TA (doubles)
-  unsigned m;       // 0x80000000 when mirrored
-};
-
-template <int TA, int NH>
-__device__ __forceinline__ void row_load(const RowRef& r, int a, double& re, double& im) {
-  const double* q = r.p + a * r.step;
-  re = q[0];
-  im = q[NH * TA];
-  const unsigned odd = (a & 1) ? 0xffffffffu : 0u;
-  re = flip_sign(re, r.m & odd);
-  im = flip_sign(im, r.m & ~odd);
-}
-
-template <int TA, int NH>
-__device__ __forceinline__ RowRef make_row(const double* sV, int ln, int base, int t, bool mir) {
-  RowRef r;
-  r.p = sV + (size_t)(base + (mir ? t : 0)) * TA + ln;
-  r.step = mir ? -TA : TA;
-  r.m = mir ? 0x80000000u : 0u;
-  return r;
-}
-
-template <int T, int TA, int L>
-__device__ __forceinline__ void y_row_items(const double* __restrict__ sV, int ln, int sub,
-                                            const YArgs& A, int it0, int it1, double (&ar)[L],
-                                            double (&ai)[L]) {
-  constexpr int NH = c_half_off(T + 1);
-  constexpr int SUB = 32 / TA;
-  for (int it = it0; it < it1; ++it) {
-    const int4 m = __ldg(A.items + it);
-    const double w = __ldg(A.itw + it);
-    const int J1 = m.z & 0xff, J2 = (m.z >> 8) & 0xff, D = (m.z >> 16) & 0xff;
-    const bool m1 = (m.z >> 24) & 1, m2 = (m.z >> 25) & 1;
-    const int JW = (m.z >> 26) & 0x1f;  // coefficient row length (j+1)
-    const RowRef r1 = make_row<TA, NH>(sV, ln, m.x, J1, m1);
-    const RowRef r2 = make_row<TA, NH>(sV, ln, m.y, J2, m2);
-    const double* cw = A.cw + m.w;
-    // window: W[ma] = x1[ma + D - a2], a2 starting at `sub`
-    double wr[L], wi[L];
-#pragma unroll
-    for (int ma = 0; ma < L; ++ma) {
-      const int a1 = min(max(ma + D - sub, 0), J1);
-      row_load<TA, NH>(r1, a1, wr[ma], wi[ma]);
-    }
-    for (int a2 = sub; a2 <= J2; a2 += SUB) {
-      double x2r, x2i;
-      row_load<TA, NH>(r2, a2, x2r, x2i);
-      x2r *= w;
-      x2i *= w;
-      const double* c = cw + a2 * JW;
-#pragma unroll
-      for (int ma = 0; ma < L; ++ma) {
-        const double cc = __ldg(c + ma);
-        const double pr = wr[ma] * x2r - wi[ma] * x2i;
-        const double pi = wr[ma] * x2i + wi[ma] * x2r;
-        ar[ma] = fma(cc, pr, ar[ma]);
-        ai[ma] = fma(cc, pi, ai[ma]);
-      }
-      // slide the window by SUB
-#pragma unroll
-      for (int ma = L - 1; ma >= SUB; --ma) {
-        wr[ma] = wr[ma - SUB];
-        wi[ma] = wi[ma - SUB];
-      }
-#pragma unroll
-      for (int ma = 0; ma < SUB && ma < L; ++ma) {
-        const int a1 = min(max(ma + D - a2 - SUB, 0), J1);
-        row_load<TA, NH>(r1, a1, wr[ma], wi[ma]);
-      }
-    }
-  }
-}
-
-// One target row (j, mb), cooperatively: the row's row-pair items are dealt
-// round-robin to the CTA's warps (all warps run the same loop body), partial
-// rows meet in shared memory, and each warp finishes a stripe of the outputs.
-template <int T, int TA, int J, bool MID>
-__device__ __forceinline__ void y_row(const double* __restrict__ sV, double* __restrict__ sred,
-                                      int lane, int w, int nw, int mb, const YArgs& A, int rid,
-                                      double* __restrict__ Yt, double& e_acc) {
-  constexpr int NH = c_half_off(T + 1);
-  constexpr int L = MID ? J / 2 + 1 : J + 1;
-  const int ln = lane % TA, sub = lane / TA;
-  double ar[L], ai[L];
-#pragma unroll
-  for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
-  const int b = __ldg(A.row_begin + rid), e = __ldg(A.row_begin + rid + 1);
-  for (int it = b + w; it < e; it += nw) y_row_items<T, TA, L>(sV, ln, sub, A, it, it + 1, ar, ai);
-#pragma unroll
-  for (int o = TA; o < 32; o <<= 1)
-#pragma unroll
-    for (int m = 0; m < L; ++m) {
-      ar[m] += __shfl_xor_sync(0xffffffffu, ar[m], o);
-      ai[m] += __shfl_xor_sync(0xffffffffu, ai[m], o);
-    }
-  // partial rows -> shared: sred[w][m][re|im][32]
-#pragma unroll
-  for (int m = 0; m < L; ++m) {
-    sred[((w * L + m) * 2 + 0) * 32 + lane] = ar[m];
-    sred[((w * L + m) * 2 + 1) * 32 + lane] = ai[m];
-  }
-  __syncthreads();
-  const int hb = c_half_off(J) + mb * (J + 1);
-  for (int ma = w; ma <= J; ma += nw) {
-    double yr = 0.0, yi = 0.0;
-    if (ma < L) {
-      for (int q = 0; q < nw; ++q) {
-        yr += sred[((q * L + ma) * 2 + 0) * 32 + lane];
-        yi += sred[((q * L + ma) * 2 + 1) * 32 + lane];
-      }
-      const double wgt = (MID && 2 * ma == J) ? 0.5 : 1.0;
-      yr *= wgt;
-      yi *= wgt;
-      if (sub == 0)
-        e_acc += yr * sV[(hb + ma) * TA + ln] + yi * sV[(NH + hb + ma) * TA + ln];
-    }
-    if (sub == 0) {
-      reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
-    }
-  }
-  __syncthreads();
-}
-
-constexpr int kYWinWarps = 12;  // max warps per k_compute_Y CTA
-
-template <int T, int TA>
-__global__ void __launch_bounds__(kYWinWarps * 32) k_compute_Y(const YArgs A) {
-  constexpr int NH = c_half_off(T + 1);
-  extern __shared__ double smem[];
-  double* sV = smem;                   // [re|im][half idx][TA atoms]
-  double* sred = smem + 2 * NH * TA;   // [warp][T+1][re|im][32]
-  __shared__ double se[kYWinWarps][32];
-  const int atom0 = blockIdx.x * TA;
-  const double* Vt = A.V + (size_t)(atom0 >> 5) * 2 * NH * 32 + (atom0 & 31);
-  for (int e = threadIdx.x; e < 2 * NH * TA; e += blockDim.x) {
-    const int row = e / TA, ln = e - row * TA;  // row = plane*NH + idx
-    sV[e] = Vt[(size_t)row * 32 + ln];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int* tasks = A.tasks + (size_t)blockIdx.y * A.task_cap;
-  const int atom = atom0 + (lane % TA);
-  double* Yt = A.Y + (size_t)atom * NH * 2;  // Y' atom-major, interleaved complex
-  double e_acc = 0.0;
-  for (int q = 0;; ++q) {
-    const int code = __ldg(tasks + q);
-    if (code < 0) break;
-    const int j = code >> 6, mb = code & 63;
-    const int rid = c_acc_off(j) + mb;  // rows enumerated (j, mb <= j/2)
-    const bool mid = 2 * mb == j;
-#define YROW(JJ)                                                                        \
-  case JJ:                                                                              \
-    if constexpr (JJ <= T) {                                                            \
-      if (mid) y_row<T, TA, JJ, true>(sV, sred, lane, w, nw, mb, A, rid, Yt, e_acc);   \
-      else y_row<T, TA, JJ, false>(sV, sred, lane, w, nw, mb, A, rid, Yt, e_acc);      \
-    }                                                                                   \
-    break;
-    switch (j) {
-      YROW(0) YROW(1) YROW(2) YROW(3) YROW(4) YROW(5) YROW(6) YROW(7)
-      YROW(8) YROW(9) YROW(10) YROW(11) YROW(12) YROW(13) YROW(14)
-      default: break;
-    }
-#undef YROW
-  }
-  // per-atom energy: fixed-order sum over the warps (deterministic)
-  se[w][lane] = e_acc;
-  __syncthreads();
-  if (w == 0) {
-    double s = 0.0;
-    for (int q = 0; q < nw; ++q) s += se[q][lane];
-    energy_epilogue(A.E, (2.0 / 3.0) * s, lane < TA && atom < A.nlocal, atom);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    *E.etotal = acc;
+    *E.ticket = 0u;
   }
 }
 
@@ -942,6 +738,7 @@ __global__ void __launch_bounds__(kYWinWarps * 32) k_compute_Y(const YArgs A) {
 #endif
 constexpr int kQPad = 16;  // X pad: window reads reach J2+1 <= 15 below, D <= 14 above
 constexpr int kQWarps = 12;
+constexpr int kQGroups = 3;  // independent warp groups per quad-unit CTA
 
 struct YQArgs {
   const double* V;
@@ -1151,7 +948,7 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs
     s += __shfl_xor_sync(0xffffffffu, s, 8);
     s += __shfl_xor_sync(0xffffffffu, s, 16);
     const int atom = atom0 + a;
-    energy_epilogue(A.E, (2.0 / 3.0) * s, lane < 8 && atom < A.nlocal, atom);
+    energy_epilogue<8>(A.E, (2.0 / 3.0) * s, lane < 8 && atom < A.nlocal, atom);
   }
 }
 
@@ -1188,6 +985,7 @@ constexpr int kXPad = 12;
 #define SNAP_Y_WARPS 12
 #endif
 constexpr int kYWarps = SNAP_Y_WARPS;  // warps per k_compute_Y_cwin CTA
+constexpr int kMaxYParts = 8;         // CTAs per tile (row split) at most
 // A CTA runs as GR independent groups of kYWarps/GR warps: GR = 3 (large
 // problems: a group owns whole target rows, with its own row list, named
 // barrier and slice of the partial-row buffer, so rows synchronise 4 warps
@@ -1518,7 +1316,7 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     double s = 0.0;
     for (int q = 0; q < nw; ++q) s += se[q][lane];
     const int atom = tile * 32 + lane;
-    energy_epilogue(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
+    energy_epilogue<32>(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
 #ifdef SNAP_Y_PROFILE
     if (lane == 0 && A.prof) {
       atomicAdd(reinterpret_cast<unsigned long long*>(A.prof) + 62,
@@ -1539,241 +1337,45 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
 
 #endif  // SNAP_T <= 8
 
+
 // ===========================================================================
 // compute_fused_dE  (snap_core.hpp:1274-1406): compute_dU fused with
-// compute_deidrj.  Lanes = (pair, row mb): a group of G lanes walks one pair,
-// lane r owning row r of the current level (v and NDIR gradient rows in
-// registers, T+1 columns).  Rows advance in place (the recursion is local to
-// a row); a new middle row at even level t is seeded from the mirror of
-// row t/2-1 (one shfl_up per column); the last middle row (level T, even T)
-// is produced transiently by the lane holding row T/2-1 and contracted at
-// once.  Each element is contracted against Y' as soon as it exists, so
-// neither u, du nor dU ever leaves registers.  dE(pair) = 2 (dsf Au + sfac Ad).
-// ===========================================================================
-struct DEArgs {
-  PairArgs pr;
-  GeoParams gp;
-  const double* Y;  // Y' stored
-  double* dedr;     // [nlocal*stride][3]
-  double* forces;   // natoms_total x 3, or null: fused scatter (snap_core.hpp:1380-1388)
-  int nslots;       // nlocal*stride
-};
-
-template <int T>
-struct DECfg {
-  static constexpr int NL = T == 0 ? 1 : ((T & 1) == 0 ? T / 2 : (T + 1) / 2);
-  static constexpr int G = NL <= 1 ? 1 : NL <= 2 ? 2 : NL <= 4 ? 4 : NL <= 8 ? 8 : 16;
-  static constexpr int PPW = 32 / G;
-  static constexpr int NC = T + 1;
-  static constexpr int NH = c_half_off(T + 1);
-  static constexpr int NDIR = T <= 8 ? 3 : 1;
-  static constexpr int WARPS = 4;
-};
-
-template <int T>
-__global__ void __launch_bounds__(DECfg<T>::WARPS * 32, (T <= 8 ? 2 : 3))
-    k_fused_dE(const DEArgs A) {
-  using C = DECfg<T>;
-  if (pipeline_failed(A.pr)) return;
-  constexpr int NDIR = C::NDIR;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = lane % C::G, q = lane / C::G;
-  const int p = (blockIdx.x * C::WARPS + w) * C::PPW + q;
-  const int S = A.pr.stride;
-  const int i = p / S, k = p - i * S;
-  const bool valid = (p < A.nslots) && (k < A.pr.numneigh[min(i, A.pr.nlocal - 1)]);
-  double x = 1.0, y = 0.0, z = 0.0, wt = 0.0;
-  if (valid) {
-    const double* d = A.pr.disp + (size_t)p * 3;
-    x = d[0];
-    y = d[1];
-    z = d[2];
-    wt = neighbor_weight(A.pr, A.pr.nbr[p]);
-  }
-  PairGeo g;
-  pair_geometry<true>(x, y, z, wt, A.gp, g);
-  const int ia = valid ? i : 0;
-  const double2* Y2 = reinterpret_cast<const double2*>(A.Y) + (size_t)ia * C::NH;
-
-  double Au = (r == 0) ? __ldg(Y2).x : 0.0;  // level 0: v = 1
-  double Ad[3] = {0.0, 0.0, 0.0};
-  const double ar = g.ar, ai = g.ai, br = g.br, bi = g.bi;
-
-  for (int pass = 0; pass < 3 / NDIR; ++pass) {
-    double dar[NDIR], dai[NDIR], dbr[NDIR], dbi[NDIR];
-#pragma unroll
-    for (int d = 0; d < NDIR; ++d) {
-      const int dd = pass * NDIR + d;
-      dar[d] = g.dar[dd];
-      dai[d] = g.dai[dd];
-      dbr[d] = g.dbr[dd];
-      dbi[d] = g.dbi[dd];
-    }
-    double vr[C::NC], vi[C::NC], dvr[NDIR][C::NC], dvi[NDIR][C::NC];
-#pragma unroll
-    for (int c = 0; c < C::NC; ++c) {
-      vr[c] = vi[c] = 0.0;
-#pragma unroll
-      for (int d = 0; d < NDIR; ++d) dvr[d][c] = dvi[d][c] = 0.0;
-    }
-    vr[0] = (r == 0) ? 1.0 : 0.0;
-    double au = 0.0, ad[NDIR];
-#pragma unroll
-    for (int d = 0; d < NDIR; ++d) ad[d] = 0.0;
-
-#pragma unroll
-    for (int t = 1; t <= T; ++t) {
-      // (1) seed a new middle row (row t/2) from the mirror of row t/2-1
-      if ((t & 1) == 0 && t < T + ((T & 1) ? 1 : 0)) {
-        const bool creator = (2 * r == t);
-        const double R = mirror_R(t);
-#pragma unroll
-        for (int c = 0; c < t; ++c) {
-          const double K = (((c + t / 2) & 1) ? -R : R);
-          const double sr = __shfl_up_sync(0xffffffffu, vr[t - 1 - c], 1);
-          const double si = __shfl_up_sync(0xffffffffu, vi[t - 1 - c], 1);
-          if (creator) {
-            vr[c] = K * sr;
-            vi[c] = -K * si;
-          }
-#pragma unroll
-          for (int d = 0; d < NDIR; ++d) {
-            const double dsr = __shfl_up_sync(0xffffffffu, dvr[d][t - 1 - c], 1);
-            const double dsi = __shfl_up_sync(0xffffffffu, dvi[d][t - 1 - c], 1);
-            if (creator) {
-              dvr[d][c] = K * dsr;
-              dvi[d][c] = -K * dsi;
-            }
-          }
-        }
-      }
-      // (2) transient last middle row (level T, even T): lane T/2-1, from its
-      //     own level T-1 row before the in-place update
-      if (t == T && (T & 1) == 0) {
-        if (2 * r + 2 == T) {
-          const double R = mirror_R(T);
-          const int hb = c_half_off(T) + (T / 2) * (T + 1);
-          double plr = 0.0, pli = 0.0, dplr[NDIR], dpli[NDIR];
-#pragma unroll
-          for (int d = 0; d < NDIR; ++d) dplr[d] = dpli[d] = 0.0;
-#pragma unroll
-          for (int c = 0; c <= T / 2; ++c) {
-            double pr = 0.0, pi = 0.0, dpr[NDIR], dpi[NDIR];
-            const double K = (((c + T / 2) & 1) ? -R : R);
-#pragma unroll
-            for (int d = 0; d < NDIR; ++d) dpr[d] = dpi[d] = 0.0;
-            if (c <= T - 1) {
-              pr = K * vr[T - 1 - c];
-              pi = -K * vi[T - 1 - c];
-#pragma unroll
-              for (int d = 0; d < NDIR; ++d) {
-                dpr[d] = K * dvr[d][T - 1 - c];
-                dpi[d] = -K * dvi[d][T - 1 - c];
-              }
-            }
-            const double nr = ar * pr + ai * pi - br * plr - bi * pli;
-            const double ni = ar * pi - ai * pr - br * pli + bi * plr;
-            const double2 yv = __ldg(Y2 + hb + c);
-            const double yr = yv.x, yi = yv.y;
-            if (pass == 0) au += nr * yr + ni * yi;
-#pragma unroll
-            for (int d = 0; d < NDIR; ++d) {
-              const double ndr = dar[d] * pr + dai[d] * pi + ar * dpr[d] + ai * dpi[d] -
-                                 dbr[d] * plr - dbi[d] * pli - br * dplr[d] - bi * dpli[d];
-              const double ndi = dar[d] * pi - dai[d] * pr + ar * dpi[d] - ai * dpr[d] -
-                                 dbr[d] * pli + dbi[d] * plr - br * dpli[d] + bi * dplr[d];
-              ad[d] += ndr * yr + ndi * yi;
-              dplr[d] = dpr[d];
-              dpli[d] = dpi[d];
-            }
-            plr = pr;
-            pli = pi;
-          }
-        }
-      }
-      // (3) advance the own row in place and contract it
-      if (2 * r <= t) {
-        const int hb = c_half_off(t) + r * (t + 1);
-#pragma unroll
-        for (int c = t; c >= 0; --c) {
-          const double pr = (c < t) ? vr[c] : 0.0, pi = (c < t) ? vi[c] : 0.0;
-          const double qr = (c > 0) ? vr[c - 1] : 0.0, qi = (c > 0) ? vi[c - 1] : 0.0;
-          const double2 yv = __ldg(Y2 + hb + c);
-            const double yr = yv.x, yi = yv.y;
-#pragma unroll
-          for (int d = 0; d < NDIR; ++d) {
-            const double dpr = (c < t) ? dvr[d][c] : 0.0, dpi = (c < t) ? dvi[d][c] : 0.0;
-            const double dqr = (c > 0) ? dvr[d][c - 1] : 0.0, dqi = (c > 0) ? dvi[d][c - 1] : 0.0;
-            const double ndr = dar[d] * pr + dai[d] * pi + ar * dpr + ai * dpi - dbr[d] * qr -
-                               dbi[d] * qi - br * dqr - bi * dqi;
-            const double ndi = dar[d] * pi - dai[d] * pr + ar * dpi - ai * dpr - dbr[d] * qi +
-                               dbi[d] * qr - br * dqi + bi * dqr;
-            dvr[d][c] = ndr;
-            dvi[d][c] = ndi;
-            ad[d] += ndr * yr + ndi * yi;
-          }
-          const double nr = ar * pr + ai * pi - br * qr - bi * qi;
-          const double ni = ar * pi - ai * pr - br * qi + bi * qr;
-          vr[c] = nr;
-          vi[c] = ni;
-          if (pass == 0) au += nr * yr + ni * yi;
-        }
-      }
-    }
-    if (pass == 0) Au += au;
-#pragma unroll
-    for (int d = 0; d < NDIR; ++d) Ad[pass * NDIR + d] += ad[d];
-  }
-  // reduce the G row-lanes of the pair
-#pragma unroll
-  for (int o = 1; o < C::G; o <<= 1) {
-    Au += __shfl_xor_sync(0xffffffffu, Au, o);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) Ad[d] += __shfl_xor_sync(0xffffffffu, Ad[d], o);
-  }
-  if (valid && r == 0) {
-    double* o = A.dedr + (size_t)p * 3;
-    double de[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      de[d] = 2.0 * (g.dsf[d] * Au + g.sfac * Ad[d]);
-      o[d] = de[d];
-    }
-    if (A.forces) {  // F_i += dE, F_nbr -= dE
-      double* fi = A.forces + (size_t)(A.pr.atom_lo + i) * 3;
-      double* fj = A.forces + (size_t)A.pr.nbr[p] * 3;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        atomicAdd(fi + d, de[d]);
-        atomicAdd(fj + d, -de[d]);
-      }
-    }
-  }
-}
-
-// ===========================================================================
-// compute_fused_dE, reverse mode.
+// compute_deidrj, by reverse-mode differentiation.
 //
-// Same (pair, row) lane layout as k_fused_dE, but the Cartesian gradient is
-// obtained by reverse-mode differentiation of the contraction
+// Lanes = (pair, row mb): a group of G lanes walks one pair, lane r owning
+// row r of the current level (T+1 columns in registers).  The Cartesian
+// gradient of the contraction
 //     F = Re sum_{t,e} conj(Y'_t(e)) v_t(e)                (v-space, stored Y')
-// instead of three forward derivative stacks (the reference's
-// wigner_du_level_half, angular_basis.hpp:262-296).  Forward sweep: v level by
-// level in registers, each row's level inputs (its own previous row, or the
-// mirrored seed of a new middle row) saved in lane-private shared memory, F
-// accumulated.  Backward sweep (level 2J..1): adjoints
+// comes from its adjoint instead of three forward derivative stacks (the
+// reference's wigner_du_level_half, angular_basis.hpp:262-296).  Forward
+// sweep: v level by level in registers, each row's level inputs (its own
+// previous row, or the mirrored seed of a new middle row) saved in
+// lane-private shared memory.  Backward sweep (level 2J..1): adjoints
 //     lambda_t(r,c) = Y'_t(r,c) + a lambda_{t+1}(r,c) - b lambda_{t+1}(r,c+1)
 // (+ the conjugated mirror adjoint of a middle row created at t+1, handed
 // down one lane), with the two complex parameter gradients
 //     G_a += conj(lambda_t(c)) P_t(c),  G_b -= conj(lambda_t(c)) P_t(c-1).
 // Then dF/dx_d = Re(conj(G_a) da_d) + Re(conj(G_b) db_d) and
 //     dE_d = 2 (dsf_d F + sfac dF/dx_d)        (snap_core.hpp:1331-1374).
-// ~30 FP64 instructions per element instead of ~64, and one complex row of
-// registers instead of four.
+// ~30 FP64 instructions per element instead of ~64 for three forward du
+// stacks, and one complex row of registers instead of four.  dU (387 MB at
+// 2000 atoms in the staged reference) never exists; the kernel writes dElist
+// only, and forces are gathered deterministically afterwards
+// (k_gather_forces).
 // ===========================================================================
+struct DEArgs {
+  PairArgs pr;
+  GeoParams gp;
+  const double* Y;  // Y' stored
+  double* dedr;     // [nlocal*stride][3]
+  int nslots;       // nlocal*stride
+};
+
 template <int T>
 struct DERCfg {
-  static constexpr int NL = DECfg<T>::NL, G = DECfg<T>::G, PPW = DECfg<T>::PPW;
+  static constexpr int NL = T == 0 ? 1 : ((T & 1) == 0 ? T / 2 : (T + 1) / 2);
+  static constexpr int G = NL <= 1 ? 1 : NL <= 2 ? 2 : NL <= 4 ? 4 : NL <= 8 ? 8 : 16;
+  static constexpr int PPW = 32 / G;
   static constexpr int NC = T + 1;
   static constexpr int NH = c_half_off(T + 1);
   static constexpr int NIN = T * (T + 1) / 2 > 0 ? T * (T + 1) / 2 : 1;  // inputs of row 0
@@ -1972,47 +1574,165 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
       de[d] = 2.0 * (g.dsf[d] * F + g.sfac * dF);
       o[d] = de[d];
     }
-    if (A.forces) {
-      double* fi = A.forces + (size_t)(A.pr.atom_lo + i) * 3;
-      double* fj = A.forces + (size_t)A.pr.nbr[p] * 3;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        atomicAdd(fi + d, de[d]);
-        atomicAdd(fj + d, -de[d]);
-      }
-    }
   }
 }
 
 #ifndef SNAP_T  // non-template kernels: host translation unit only
 // ===========================================================================
-// scatter_forces (snap_core.hpp:872-953, concurrent-RMW strategy):
-// F_i += dE(i,k), F_{nbr} -= dE(i,k) with FP64 RED atomics.
+// scatter_forces (snap_core.hpp:872-953), deterministic.
+//
+// The reference's deterministic mode walks the pairs serially in canonical
+// order, F_i += dE(i,k), F_nbr(i,k) -= dE(i,k) (:889-899).  Here each force
+// component is owned by one thread that PULLS its contributions in exactly
+// that order: the pairs (i,k) with nbr(i,k) = a come from a reverse-neighbor
+// index (CSR over atoms, slots sorted), merged with the atom's own row by
+// pair index.  So the force of atom a is the reference's floating-point sum,
+// term for term, of the dElist it is given, and it is bitwise reproducible.
+//
+// The reverse index is rebuilt only when the lists change
+// (k_rev_count -> k_nl_scan -> k_rev_fill -> k_rev_sort).
 // ===========================================================================
-struct ScatterArgs {
+struct RevArgs {
   PairArgs pr;
-  const double* dedr;
-  double* forces;  // natoms_total x 3
+  int* off;   // [natoms_total + 1]: counts at off[a+1], then exclusive offsets
+  int* cur;   // [natoms_total]: fill cursors (= offsets after the scan)
+  int* rev;   // [valid pairs]: local slot index p = i*stride + k, grouped by neighbor
   int nslots;
 };
 
-__global__ void __launch_bounds__(256) k_scatter_forces(const ScatterArgs A) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= A.nslots || pipeline_failed(A.pr)) return;
-  const int S = A.pr.stride;
+// a valid pair's neighbor, or -1 (malformed lists are flagged by compute_U)
+__device__ __forceinline__ int rev_target(const PairArgs& A, int p) {
+  const int S = A.stride;
   const int i = p / S, k = p - i * S;
-  if (k >= A.pr.numneigh[i]) return;
-  const int j = A.pr.nbr[p];
-  const double* de = A.dedr + (size_t)p * 3;
-  const double d0 = de[0], d1 = de[1], d2 = de[2];
-  double* fi = A.forces + (size_t)(A.pr.atom_lo + i) * 3;
-  double* fj = A.forces + (size_t)j * 3;
-  atomicAdd(fi + 0, d0);
-  atomicAdd(fi + 1, d1);
-  atomicAdd(fi + 2, d2);
-  atomicAdd(fj + 0, -d0);
-  atomicAdd(fj + 1, -d1);
-  atomicAdd(fj + 2, -d2);
+  const int nn = A.numneigh[i];
+  if (nn < 0 || nn > S || k >= nn) return -1;
+  const int j = A.nbr[p];
+  return (j >= 0 && j < A.natoms_total) ? j : -1;
+}
+
+__global__ void __launch_bounds__(256) k_rev_count(const RevArgs A) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.nslots) return;
+  const int j = rev_target(A.pr, p);
+  if (j >= 0) atomicAdd(A.off + j + 1, 1);
+}
+
+__global__ void __launch_bounds__(256) k_rev_fill(const RevArgs A) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.nslots) return;
+  const int j = rev_target(A.pr, p);
+  if (j >= 0) A.rev[atomicAdd(A.cur + j, 1)] = p;
+}
+
+// each atom's reverse slots in ascending pair order (the fill order is
+// racy): one warp per atom, every lane ranks one slot against the others
+// (slots are distinct), longer segments 32 at a time by a serial merge
+__global__ void __launch_bounds__(256) k_rev_sort(const RevArgs A) {
+  const int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (a >= A.pr.natoms_total) return;
+  int* r = A.rev + A.off[a];
+  const int m = A.off[a + 1] - A.off[a];
+  if (m <= 32) {
+    const int v = lane < m ? r[lane] : INT32_MAX;
+    int rank = 0;
+    for (int q = 0; q < m; ++q) rank += (__shfl_sync(0xffffffffu, v, q) < v) ? 1 : 0;
+    __syncwarp();
+    if (lane < m) r[rank] = v;
+    return;
+  }
+  if (lane == 0)
+    for (int x = 1; x < m; ++x) {  // rare: more than 32 reverse pairs
+      const int v = r[x];
+      int y = x - 1;
+      while (y >= 0 && r[y] > v) {
+        r[y + 1] = r[y];
+        --y;
+      }
+      r[y + 1] = v;
+    }
+}
+
+// Force output layout: atom a, component d at
+//     (a / chunk_rows) * chunk_stride + (a % chunk_rows) * 3 + d.
+// One chunk (chunk_rows = natoms_total) is the plain [atom][3] array.  The
+// multi-GPU layout has one chunk per rank, each followed by an energy slot
+// that receives this rank's total energy, so a single reduce-scatter sums
+// both the partial forces and the energies (distributed.py).
+struct GatherArgs {
+  PairArgs pr;
+  const int* off;
+  const int* rev;
+  const double* dedr;
+  double* forces;
+  int chunk_rows, chunk_stride, nchunks;
+  const double* etotal;  // this rank's total (nchunks > 1)
+};
+
+// One warp per atom: the lanes fetch 32 terms of the atom's merged sequence
+// at a time (reverse slots before its own row, its own row, the remaining
+// reverse slots) with independent loads, then every lane adds them in
+// sequence order (the serialized order of snap_core.hpp:889-899; a - x and
+// a + (-x) round identically).
+__global__ void __launch_bounds__(256) k_gather_forces(const GatherArgs A) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (A.nchunks > 1 && blockIdx.x == 0 && threadIdx.x < A.nchunks)
+    A.forces[(size_t)threadIdx.x * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
+  const int a = gw;
+  if (a >= A.pr.natoms_total) return;
+  double* fo = A.forces + (size_t)(a / A.chunk_rows) * A.chunk_stride + (size_t)(a % A.chunk_rows) * 3;
+  if (pipeline_failed(A.pr)) {
+    if (lane < 3) fo[lane] = 0.0;
+    return;
+  }
+  const int S = A.pr.stride;
+  const int s0 = A.off[a], nrev = A.off[a + 1] - s0;
+  const int il = a - A.pr.atom_lo;
+  int nn = 0, own = 0;
+  if (il >= 0 && il < A.pr.nlocal) {
+    own = il * S;
+    nn = A.pr.numneigh[il];
+    nn = (nn < 0 || nn > S) ? 0 : nn;
+  }
+  // reverse slots that precede the own row (the slots are sorted)
+  int nbefore = 0;
+  if (nn > 0)
+    for (int b = 0; b < nrev; b += 32) {
+      const bool lt = (b + lane < nrev) && (A.rev[s0 + b + lane] < own);
+      nbefore += __popc(__ballot_sync(0xffffffffu, lt));
+    }
+  const int M = nrev + nn;
+  double fx = 0.0, fy = 0.0, fz = 0.0;
+  for (int b = 0; b < M; b += 32) {
+    const int q = b + lane;
+    double vx = 0.0, vy = 0.0, vz = 0.0;
+    if (q < M) {
+      int p;
+      double sg = -1.0;
+      if (q < nbefore) {
+        p = A.rev[s0 + q];
+      } else if (q < nbefore + nn) {
+        p = own + (q - nbefore);
+        sg = 1.0;
+      } else {
+        p = A.rev[s0 + q - nn];
+      }
+      const double* de = A.dedr + (size_t)p * 3;
+      vx = sg * de[0];
+      vy = sg * de[1];
+      vz = sg * de[2];
+    }
+    const int cnt = min(32, M - b);
+    for (int t = 0; t < cnt; ++t) {
+      fx += __shfl_sync(0xffffffffu, vx, t);
+      fy += __shfl_sync(0xffffffffu, vy, t);
+      fz += __shfl_sync(0xffffffffu, vz, t);
+    }
+  }
+  if (lane == 0) {
+    fo[0] = fx;
+    fo[1] = fy;
+    fo[2] = fz;
+  }
 }
 
 // ===========================================================================
@@ -2218,20 +1938,6 @@ __global__ void __launch_bounds__(128) k_nl_lists(const NLArgs A) {
     A.disp[pk * 3 + 1] = nl_min_image(__dsub_rn(A.w[k * 3 + 1], yi), A.box[1]);
     A.disp[pk * 3 + 2] = nl_min_image(__dsub_rn(A.w[k * 3 + 2], zi), A.box[2]);
   }
-}
-
-// Deterministic total energy: one CTA, fixed-order tree over eatom.
-__global__ void __launch_bounds__(1024) k_energy_total(const double* eatom, int n, double* out) {
-  __shared__ double red[1024];
-  double s = 0.0;
-  for (int a = threadIdx.x; a < n; a += blockDim.x) s += eatom[a];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = red[0];
 }
 
 // FP64 issue-rate probe: 8 independent DFMA chains per thread.

@@ -21,7 +21,7 @@ template <int T>
 static L2Prefetch y_prefetch(snapgpu_ctx* c) {
   L2Prefetch P{};
 #if SNAP_T <= 8
-  if (c->y_impl == 0) {
+  {
     void* a[4] = {nullptr, nullptr, nullptr, nullptr};
     CK(cudaGetSymbolAddress(&a[0], cCW));
     CK(cudaGetSymbolAddress(&a[1], cYItems4));
@@ -61,169 +61,104 @@ static void launch_U2(snapgpu_ctx* c) {
 
 template <int T>
 void launch_U_t(snapgpu_ctx* c) {
-  if constexpr (T <= 8) {
-    if (c->u_impl == 0) {  // row-lane kernel
-      // two pair slots per atom when the atoms fill the SMs, else four
-      // (measured at 2000 atoms: 2 / 4 / 8 slots -> 28.7 / 26.4 / 31.6 us)
-      int nsm = 148;
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-      int sl = (c->nlocal / U2Cfg<T, 2>::APW >= 8 * nsm) ? 2 : 4;
-      if (const char* e = std::getenv("SNAPGPU_U_SLOTS")) sl = std::atoi(e);  // development A/B
-      if (sl == 2) return launch_U2<T, 2>(c);
-      if (sl == 4) return launch_U2<T, 4>(c);
-      return launch_U2<T, 8>(c);
-    }
-  }
-  using C = UCfg<T>;
-  UArgs a;
-  a.pr = pair_args(c);
-  a.gp = c->gp;
-  a.V = c->d_V.p;
-  a.pf = L2Prefetch{};
-  const size_t smem = sizeof(double) * ((size_t)C::WARPS * c->stride * 5 +
-                                        (C::REGACC ? 0 : (size_t)C::WARPS * 2 * C::NACC * 32));
-  static bool attr = false;
-  if (!attr || smem > 48 * 1024) {
+  if constexpr (T <= 8) {  // row-lane kernel
+    // two pair slots per atom when the atoms fill the SMs, else four
+    // (measured at 2000 atoms: 2 / 4 / 8 slots -> 28.7 / 26.4 / 31.6 us)
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    if (c->nlocal / U2Cfg<T, 2>::APW >= 8 * nsm) return launch_U2<T, 2>(c);
+    return launch_U2<T, 4>(c);
+  } else {  // column-lane kernel
+    using C = UCfg<T>;
+    UArgs a;
+    a.pr = pair_args(c);
+    a.gp = c->gp;
+    a.V = c->d_V.p;
+    a.pf = L2Prefetch{};
+    const size_t smem = sizeof(double) * ((size_t)C::WARPS * c->stride * 5 +
+                                          (C::REGACC ? 0 : (size_t)C::WARPS * 2 * C::NACC * 32));
     CK(cudaFuncSetAttribute(k_compute_U<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = true;
+    const int blocks = (c->nlocal + C::WARPS - 1) / C::WARPS;
+    k_compute_U<T><<<blocks, C::WARPS * 32, smem, c->stream>>>(a);
+    CK(cudaGetLastError());
   }
-  const int blocks = (c->nlocal + C::WARPS - 1) / C::WARPS;
-  k_compute_U<T><<<blocks, C::WARPS * 32, smem, c->stream>>>(a);
-  CK(cudaGetLastError());
-}
-
-template <int T, int TA>
-static void launch_Y_window(snapgpu_ctx* c) {
-  constexpr int NH = c_half_off(T + 1);
-  YArgs a;
-  a.V = c->d_V.p;
-  a.Y = c->d_Y.p;
-  a.items = c->d_items.p;
-  a.itw = c->d_itw.p;
-  a.row_begin = c->d_rowbeg.p;
-  a.cw = c->d_cw.p;
-  a.tasks = c->d_tasks.p;
-  a.task_cap = c->task_cap;
-  a.nlocal = c->nlocal;
-  a.E = energy_out(c);
-  const size_t smem = sizeof(double) * (2 * NH * TA + (size_t)c->y_warps * (T + 1) * 2 * 32);
-  CK(cudaFuncSetAttribute(k_compute_Y<T, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  dim3 grid((c->ntiles * 32) / TA, c->y_parts_used);
-  k_compute_Y<T, TA><<<grid, c->y_warps * 32, smem, c->stream>>>(a);
-  CK(cudaGetLastError());
 }
 
 template <int T>
 void launch_Y_t(snapgpu_ctx* c) {
-  constexpr int NH = c_half_off(T + 1);
 #if SNAP_T <= 8
-  if constexpr (cw_base(T) >= 0) {
-    if (c->y_impl == 0) {
-      constexpr int NF = c_full_off(T + 1);
-      constexpr int NP = NF + 2 * kXPad;
-      YWArgs a;
-      a.V = c->d_V.p;
-      a.Y = c->d_Y.p;
-      a.expand = c->d_expand.p;
-      a.itw = c->d_citw[c->y_groups == 3 ? 0 : 1].p;
-      a.nitems = static_cast<int>(c->ycplan[0].items.size());
-      a.prof = nullptr;
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int NP = NF + 2 * kXPad;
+  YWArgs a;
+  a.V = c->d_V.p;
+  a.Y = c->d_Y.p;
+  a.expand = c->d_expand.p;
+  a.itw = c->d_citw[c->y_groups == 3 ? 0 : 1].p;
+  a.nitems = static_cast<int>(c->ycplan[0].items.size());
+  a.prof = nullptr;
 #ifdef SNAP_Y_PROFILE
-      if (!g_yprof) {
-        CK(cudaMalloc(&g_yprof, 2112 * sizeof(long long)));
-        CK(cudaMemset(g_yprof, 0, 2112 * sizeof(long long)));
-      }
-      a.prof = g_yprof;
+  if (!g_yprof) {
+    CK(cudaMalloc(&g_yprof, 2112 * sizeof(long long)));
+    CK(cudaMemset(g_yprof, 0, 2112 * sizeof(long long)));
+  }
+  a.prof = g_yprof;
 #endif
-      a.tasks = c->d_tasks.p;
-      a.task_cap = c->task_cap;
-      a.nlocal = c->nlocal;
-      a.E = energy_out(c);
-      const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYWarps * (T + 1) * 2 * 32 +
-                                            (size_t)a.nitems);
-      dim3 grid(c->ntiles, c->y_parts_used);
-      if (c->y_groups == 3) {
-        CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 3>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_compute_Y_cwin<T, 3><<<grid, kYWarps * 32, smem, c->stream>>>(a);
-      } else {
-        CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 1>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_compute_Y_cwin<T, 1><<<grid, kYWarps * 32, smem, c->stream>>>(a);
-      }
-      CK(cudaGetLastError());
-      return;
-    }
+  a.tasks = c->d_tasks.p;
+  a.task_cap = c->task_cap;
+  a.nlocal = c->nlocal;
+  a.E = energy_out(c);
+  const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYWarps * (T + 1) * 2 * 32 +
+                                        (size_t)a.nitems);
+  dim3 grid(c->ntiles, c->y_parts_used);
+  if (c->y_groups == 3) {
+    CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    k_compute_Y_cwin<T, 3><<<grid, kYWarps * 32, smem, c->stream>>>(a);
+  } else {
+    CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    k_compute_Y_cwin<T, 1><<<grid, kYWarps * 32, smem, c->stream>>>(a);
   }
+  CK(cudaGetLastError());
+#else
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int NP = NF + 2 * kQPad;
+  YQArgs a;
+  a.V = c->d_V.p;
+  a.Y = c->d_Y.p;
+  a.expand = c->d_expand.p;
+  a.units = c->d_qunits.p;
+  a.itw = c->d_qitw.p;
+  a.rw = c->d_qrw.p;
+  a.cw = c->d_cw.p;
+  a.rows = c->d_qrows.p;
+  a.rows_cap = c->yqplan.rows_cap;
+  a.nlocal = c->nlocal;
+  a.E = energy_out(c);
+  const size_t smem = sizeof(double) * (2 * NP * 8 + (size_t)kQWarps * (T + 1) * 2 * 8);
+  CK(cudaFuncSetAttribute(k_compute_Y_quad<T, kQGroups>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_compute_Y_quad<T, kQGroups><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
+  CK(cudaGetLastError());
 #endif
-  if constexpr (T > 8) {
-    if (c->y_impl == 3) {
-      constexpr int NF = c_full_off(T + 1);
-      constexpr int NP = NF + 2 * kQPad;
-      YQArgs a;
-      a.V = c->d_V.p;
-      a.Y = c->d_Y.p;
-      a.expand = c->d_expand.p;
-      a.units = c->d_qunits.p;
-      a.itw = c->d_qitw.p;
-      a.rw = c->d_qrw.p;
-      a.cw = c->d_cw.p;
-      a.rows = c->d_qrows.p;
-      a.rows_cap = c->yqplan.rows_cap;
-      a.nlocal = c->nlocal;
-      a.E = energy_out(c);
-      const size_t smem = sizeof(double) * (2 * NP * 8 + (size_t)kQWarps * (T + 1) * 2 * 8);
-      if (c->yq_groups == 3) {
-        CK(cudaFuncSetAttribute(k_compute_Y_quad<T, 3>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_compute_Y_quad<T, 3><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
-      } else {
-        CK(cudaFuncSetAttribute(k_compute_Y_quad<T, 1>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_compute_Y_quad<T, 1><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
-      }
-      CK(cudaGetLastError());
-      return;
-    }
-  }
-  constexpr int RED = kYWinWarps * (T + 1) * 2 * 32 * 8;
-  if constexpr (2 * NH * 32 * 8 + RED <= 200 * 1024) {
-    if (c->y_ta == 32) return launch_Y_window<T, 32>(c);
-  }
-  if constexpr (2 * NH * 16 * 8 + RED <= 200 * 1024) {
-    if (c->y_ta >= 16) return launch_Y_window<T, 16>(c);
-  }
-  return launch_Y_window<T, 8>(c);
 }
 
 template <int T>
 void launch_DE_t(snapgpu_ctx* c) {
-  using C = DECfg<T>;
+  using R = DERCfg<T>;
   DEArgs a;
   a.pr = pair_args(c);
   a.gp = c->gp;
   a.Y = c->d_Y.p;
   a.dedr = c->d_dedr.p;
-  a.forces = c->fuse_scatter ? c->d_forces.p : nullptr;
   a.nslots = c->nlocal * c->stride;
-  if (c->de_impl == 0) {  // reverse mode
-    using R = DERCfg<T>;
-    const int per_block = R::WARPS * R::PPW;
-    const int blocks = (a.nslots + per_block - 1) / per_block;
-    if (blocks > 0) {
-      CK(cudaFuncSetAttribute(k_fused_dE_rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              R::SMEM));
-      k_fused_dE_rev<T><<<blocks, R::WARPS * 32, R::SMEM, c->stream>>>(a);
-      CK(cudaGetLastError());
-    }
-    return;
-  }
-  const int per_block = C::WARPS * C::PPW;
+  const int per_block = R::WARPS * R::PPW;
   const int blocks = (a.nslots + per_block - 1) / per_block;
   if (blocks > 0) {
-    k_fused_dE<T><<<blocks, C::WARPS * 32, 0, c->stream>>>(a);
+    CK(cudaFuncSetAttribute(k_fused_dE_rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            R::SMEM));
+    k_fused_dE_rev<T><<<blocks, R::WARPS * 32, R::SMEM, c->stream>>>(a);
     CK(cudaGetLastError());
   }
 }

@@ -66,48 +66,41 @@ void upload_ytables(int device, int T, const YTablesHost& t) {
              upload_ytables_t<14>)(device, t);
 }
 
-// compute_Y work split: TA atoms per CTA (32 when the V tile fits, smaller
-// tiles for small problems so the SMs fill), W warps per CTA owning target
-// rows, and P "parts" of the row list per tile when tiles are still scarce.
+// compute_Y work split (2J <= 8): one CTA per 32-atom tile, or, when the
+// tiles are too few to fill the SMs, P CTAs per tile splitting its target
+// rows (LPT on measured row costs); 2J > 8: one CTA per 8 atoms, fixed rows.
 void build_ycoop(snapgpu_ctx* c);
 
 void plan_y(snapgpu_ctx* c) {
-  if (c->y_impl == 3) return;  // quad-unit kernel: fixed row order, one CTA per 8 atoms
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  if (c->y_impl == 0) {  // one 32-atom tile per CTA, all warps per row
-    int parts = c->y_parts;
+  int parts = 1;
+  if (c->T <= 8) {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    parts = c->y_parts;
     // one CTA per SM: never exceed a single wave
-    if (parts <= 0) parts = std::max(1, std::min(8, nsm / std::max(1, c->ntiles)));
-    c->y_parts_used = parts;
+    if (parts <= 0) parts = std::max(1, std::min(kMaxYParts, nsm / std::max(1, c->ntiles)));
     // one row list per (part, warp group): three 4-warp groups when a CTA
     // owns a whole tile, one 12-warp group (finest row granularity) when the
     // tile is split over several CTAs
     c->y_groups = (parts == 1) ? 3 : 1;
-    if (const char* e = std::getenv("SNAPGPU_Y_GROUPS")) c->y_groups = std::atoi(e) == 1 ? 1 : 3;
     std::vector<int> tasks =
         y_row_schedule(c->maps, c->ycplan[0].row_cost, parts * c->y_groups, &c->task_cap);
     c->d_tasks.alloc(tasks.size());
     CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
-    return;
   }
-  int ta = c->y_ta_req > 0 ? std::min(c->y_ta_req, c->y_ta_max) : c->y_ta_max;
-  if (c->y_ta_req <= 0)
-    while (ta > 16 && (c->ntiles * 32) / ta < nsm) ta /= 2;  // small N: more, thinner CTAs
-  c->y_ta = ta;
-  const int units = (c->ntiles * 32) / ta;
-  int parts = c->y_parts;
-  if (parts <= 0) parts = std::max(1, std::min(8, (2 * nsm + units - 1) / std::max(1, units)));
   c->y_parts_used = parts;
-  const int workers = parts;  // all warps of a CTA cooperate on each row
-  std::vector<int> tasks = y_row_schedule(c->maps, c->yplan.row_cost, workers, &c->task_cap);
-  c->d_tasks.alloc(tasks.size());
-  CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
+  // energy epilogue: per-CTA lane energies, per-tile sums and tickets (the
+  // 2J > 8 kernel has 4 tiles of 8 atoms per 32-atom V tile)
+  const size_t nt = (size_t)std::max(1, c->ntiles);
+  c->d_epart.alloc((size_t)parts * nt * 32);
+  c->d_tile_sum.alloc(4 * nt);
+  c->d_tickets.alloc(1 + 4 * nt);
+  CK(cudaMemsetAsync(c->d_tickets.p, 0, sizeof(unsigned) * (1 + 4 * nt), c->stream));
 }
 
 void upload_beta(snapgpu_ctx* c) {
-  if (c->y_impl == 0) {
-    const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
+  const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
+  if (c->T <= 8) {
     for (int k = 0; k < 2; ++k) {  // item order of the 4- and 12-warp unit tables
       const std::vector<double> itw = ycoop_weights(c->ycplan[k], c->maps, W);
       c->d_citw[k].alloc(std::max<size_t>(1, itw.size()));
@@ -116,17 +109,9 @@ void upload_beta(snapgpu_ctx* c) {
     }
     return;
   }
-  if (c->y_impl == 3) {
-    const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
-    const std::vector<double> itw = yquad_weights(c->yqplan, c->maps, W);
-    c->d_qitw.alloc(std::max<size_t>(1, itw.size()));
-    CK(cudaMemcpy(c->d_qitw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
-    return;
-  }
-  const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), true);
-  const std::vector<double> itw = y_item_weights(c->maps, W);
-  c->d_itw.alloc(std::max<size_t>(1, itw.size()));
-  CK(cudaMemcpy(c->d_itw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
+  const std::vector<double> itw = yquad_weights(c->yqplan, c->maps, W);
+  c->d_qitw.alloc(std::max<size_t>(1, itw.size()));
+  CK(cudaMemcpy(c->d_qitw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
 }
 
 // constant-window units, packed for the constant bank (kernels.cuh cYItems4/12)
@@ -173,33 +158,93 @@ void launch_U(snapgpu_ctx* c) {
   if (c->nlocal > 0) SNAP_PICK(launch_U_t, c->T)(c);
 }
 void launch_Y(snapgpu_ctx* c) {
-  CK(cudaMemsetAsync(c->d_eatom.p, 0, sizeof(double) * std::max(1, c->nlocal), c->stream));
   if (c->nlocal > 0) {
-    SNAP_PICK(launch_Y_t, c->T)(c);  // energy total in the kernel's last CTA
+    SNAP_PICK(launch_Y_t, c->T)(c);  // eatom and the total from the kernel's epilogue
   } else {
     CK(cudaMemsetAsync(c->d_etotal.p, 0, sizeof(double), c->stream));
   }
 }
 void launch_dE(snapgpu_ctx* c) {
-  // Fusing the scatter into the dE kernel saves a launch for small problems;
-  // for large ones the separate RED kernel is cheaper than atomics issued
-  // from the latency-bound dE kernel.
-  c->fuse_scatter = (size_t)c->nlocal * c->stride <= (1u << 18);
-  if (c->fuse_scatter)
-    CK(cudaMemsetAsync(c->d_forces.p, 0, sizeof(double) * 3 * std::max(1, c->natoms_total),
-                       c->stream));
   if (c->nlocal > 0) SNAP_PICK(launch_DE_t, c->T)(c);
 }
-void launch_scatter(snapgpu_ctx* c) {
-  CK(cudaMemsetAsync(c->d_forces.p, 0, sizeof(double) * 3 * std::max(1, c->natoms_total),
-                     c->stream));
-  ScatterArgs a;
+
+double* forces_ptr(snapgpu_ctx* c) { return c->ext_forces ? c->ext_forces : c->d_forces.p; }
+// doubles of the force output: natoms x 3, or nchunks x (3 chunk_rows + 1)
+size_t force_doubles(const snapgpu_ctx* c) {
+  return c->natoms_total > 0 ? (size_t)c->nchunks * c->chunk_stride() : 0;
+}
+
+RevArgs rev_args(snapgpu_ctx* c) {
+  RevArgs a;
   a.pr = pair_args(c);
-  a.dedr = c->d_dedr.p;
-  a.forces = c->d_forces.p;
+  a.off = c->d_rev_off.p;
+  a.cur = c->d_rev_cur.p;
+  a.rev = c->d_rev.p;
   a.nslots = c->nlocal * c->stride;
+  return a;
+}
+
+// reverse-neighbor index of the current lists (kernels.cuh k_rev_*)
+void launch_rev_build(snapgpu_ctx* c) {
+  const int n = c->natoms_total;
+  CK(cudaMemsetAsync(c->d_rev_off.p, 0, sizeof(int) * (n + 1), c->stream));
+  const RevArgs a = rev_args(c);
   if (a.nslots > 0) {
-    k_scatter_forces<<<(a.nslots + 255) / 256, 256, 0, c->stream>>>(a);
+    const int blk = (a.nslots + 255) / 256;
+    k_rev_count<<<blk, 256, 0, c->stream>>>(a);
+    k_nl_scan<<<1, 1024, 0, c->stream>>>(a.off, n, a.cur);
+    k_rev_fill<<<blk, 256, 0, c->stream>>>(a);
+    if (n > 0) k_rev_sort<<<(n + 7) / 8, 256, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+  }
+}
+
+void invalidate_csr_graph(snapgpu_ctx* c) {
+  if (c->csr_gexec) cudaGraphExecDestroy(c->csr_gexec);
+  if (c->csr_graph) cudaGraphDestroy(c->csr_graph);
+  c->csr_gexec = nullptr;
+  c->csr_graph = nullptr;
+}
+
+// Rebuild the reverse index if the lists changed since the last build (a
+// captured graph of its five stream operations, replayed per list upload).
+void ensure_csr(snapgpu_ctx* c) {
+  if (!c->csr_dirty) return;
+  if (!c->csr_gexec) {
+    cudaStream_t user = c->stream;
+    c->stream = c->own_stream;
+    CK(cudaStreamSynchronize(user));
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      launch_rev_build(c);
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c->stream = user;
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &c->csr_graph));
+    CK(cudaGraphInstantiate(&c->csr_gexec, c->csr_graph, 0));
+    c->stream = user;
+  }
+  CK(cudaGraphLaunch(c->csr_gexec, c->stream));
+  c->csr_dirty = false;
+}
+
+void launch_gather(snapgpu_ctx* c) {
+  GatherArgs a;
+  a.pr = pair_args(c);
+  a.off = c->d_rev_off.p;
+  a.rev = c->d_rev.p;
+  a.dedr = c->d_dedr.p;
+  a.forces = forces_ptr(c);
+  a.chunk_rows = c->chunk_rows();
+  a.chunk_stride = c->chunk_stride();
+  a.nchunks = c->nchunks;
+  a.etotal = c->d_etotal.p;
+  if (c->natoms_total > 0) {  // one warp per atom
+    k_gather_forces<<<(c->natoms_total + 7) / 8, 256, 0, c->stream>>>(a);
     CK(cudaGetLastError());
   }
 }
@@ -226,13 +271,18 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
           "problem: owned range outside the atom count");
   require(nlocal == 0 || natoms_total > 0, "problem: no atoms");
   require(stride >= 0, "problem: negative neighbor stride");
+  require((size_t)nlocal * stride < (size_t)INT32_MAX / 3, "problem: too many neighbor slots");
   require(!upload || nlocal == 0 || stride == 0 || (numneigh && nbr && disp),
           "problem: null neighbor arrays");
-  c->have_lists = c->have_U = c->have_Y = c->have_dE = false;
+  c->have_lists = c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
+  c->csr_dirty = true;
   const bool reshape = natoms_total != c->natoms_total || nlocal != c->nlocal ||
                        stride != c->stride || atom_lo != c->atom_lo ||
                        (types != nullptr) != (c->d_types.p != nullptr);
-  if (reshape) invalidate_graph(c);
+  if (reshape) {
+    invalidate_graph(c);
+    invalidate_csr_graph(c);
+  }
   c->natoms_total = natoms_total;
   c->atom_lo = atom_lo;
   c->nlocal = nlocal;
@@ -246,9 +296,13 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
     c->d_nbr.alloc(std::max<size_t>(1, nslots));
     c->d_disp.alloc(std::max<size_t>(1, nslots * 3));
     c->d_dedr.alloc(std::max<size_t>(1, nslots * 3));
+    c->d_rev_off.alloc((size_t)natoms_total + 1);
+    c->d_rev_cur.alloc(std::max(1, natoms_total));
+    c->d_rev.alloc(std::max<size_t>(1, nslots));
     // forces, eatom and etotal are contiguous so the one-call API reads them
     // back with a single copy
-    const size_t nf = (size_t)std::max(1, natoms_total) * 3, ne = std::max(1, nlocal);
+    const size_t nf = (size_t)std::max(1, c->nchunks) * c->chunk_stride(),
+                 ne = std::max(1, nlocal);
     c->d_forces.release();
     c->d_eatom.release();
     c->d_etotal.release();
@@ -256,9 +310,6 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
     c->d_forces.view(c->d_out.p, nf);
     c->d_eatom.view(c->d_out.p + nf, ne);
     c->d_etotal.view(c->d_out.p + nf + ne, 1);
-    c->d_part.alloc((size_t)std::max(1, ntiles) * 4 * 8 + 64);  // >= Y grid size
-    c->d_ticket.alloc(1);
-    CK(cudaMemsetAsync(c->d_ticket.p, 0, sizeof(unsigned), c->stream));
     const bool grow = vsz > c->d_V.n;
     c->d_V.alloc(vsz);
     c->d_Y.alloc(vsz);
@@ -335,7 +386,7 @@ void run_direct(snapgpu_ctx* c) {
   record(c, 2);
   launch_dE(c);
   record(c, 3);
-  if (!c->fuse_scatter) launch_scatter(c);
+  launch_gather(c);
   record(c, 4);
 }
 
@@ -421,53 +472,24 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     };
     up(c->d_weights, c->weights);
     c->yplan = y_plan(c->maps, cprime_table(c->maps, c->cg));
-    std::vector<int4> it(c->yplan.items.size());
-    for (size_t q = 0; q < it.size(); ++q)
-      it[q] = make_int4(c->yplan.items[q][0], c->yplan.items[q][1], c->yplan.items[q][2],
-                        c->yplan.items[q][3]);
-    up(c->d_items, it);
-    up(c->d_rowbeg, c->yplan.row_begin);
-    up(c->d_cw, c->yplan.cw);
-    // compute_Y implementation: constant-window (default for 2J <= 8, where
-    // the windowed C' fits constant memory), unrolled (2J = 8), half-V window.
-    c->y_impl = (cw_base(twojmax) >= 0) ? 0 : 3;
-    c->de_impl = 0;  // reverse mode at every 2J (2J=14: 4.2 ms vs 8.6 ms forward at 32k atoms)
-    if (const char* e = std::getenv("SNAPGPU_DE_IMPL"))  // A/B switch for development
-      c->de_impl = (std::string(e) == "forward") ? 1 : 0;
-    c->u_impl = (twojmax <= 8) ? 0 : 1;
-    if (const char* e = std::getenv("SNAPGPU_U_IMPL"))  // A/B switch for development
-      if (std::string(e) == "column") c->u_impl = 1;
-    if (const char* e = std::getenv("SNAPGPU_Y_IMPL"))  // A/B switch for development
-      if (std::string(e) == "window") c->y_impl = 2;
-    if (c->y_impl == 0) {
-      c->y_warps = 12;
-      up(c->d_expand, half_scatter_map(c->maps));
-      build_ycoop(c);  // constant-bank tables + the beta-dependent item weights
+    up(c->d_expand, half_scatter_map(c->maps));
+    if (twojmax <= 8) {
+      // constant-window compute_Y: the windowed C' and the unit tables live
+      // in the per-2J object's constant bank
+      build_ycoop(c);
     } else {
-      if (c->y_impl == 3) {  // quad-unit tables (beta-independent part)
-        up(c->d_expand, half_scatter_map(c->maps));
-        c->yq_groups = 3;  // 3 groups of 4 warps (A/B: SNAPGPU_YQ_GROUPS=1)
-        if (const char* e = std::getenv("SNAPGPU_YQ_GROUPS")) c->yq_groups = std::atoi(e) == 1 ? 1 : 3;
-        c->yqplan = yquad_plan(c->maps, kQWarps / c->yq_groups, c->yq_groups);
-        std::vector<int4> u(c->yqplan.units.size());
-        for (size_t q = 0; q < u.size(); ++q)
-          u[q] = make_int4(c->yqplan.units[q][0], c->yqplan.units[q][1], c->yqplan.units[q][2],
-                           c->yqplan.units[q][3]);
-        up(c->d_qunits, u);
-        up(c->d_qrw, c->yqplan.rw);
-        up(c->d_qrows, c->yqplan.rows);
-      }
+      // quad-unit compute_Y: C' and the beta-independent unit tables in HBM
+      up(c->d_cw, c->yplan.cw);
+      c->yqplan = yquad_plan(c->maps, kQWarps / kQGroups, kQGroups);
+      std::vector<int4> u(c->yqplan.units.size());
+      for (size_t q = 0; q < u.size(); ++q)
+        u[q] = make_int4(c->yqplan.units[q][0], c->yqplan.units[q][1], c->yqplan.units[q][2],
+                         c->yqplan.units[q][3]);
+      up(c->d_qunits, u);
+      up(c->d_qrw, c->yqplan.rw);
+      up(c->d_qrows, c->yqplan.rows);
       upload_beta(c);
     }
-    const int nh = c->maps.nhalf;
-    // V tile + the cross-warp row buffer (8 warps) must fit in shared memory
-    // half-V window kernel (2J > 8): 12 warps per CTA (measured at 2J=14,
-    // 32k atoms: 4 / 6 / 8 warps -> 105 / 83 / 66 ms); the V tile + the
-    // cross-warp row buffer must fit in shared memory
-    if (c->y_impl != 0) c->y_warps = kYWinWarps;
-    const double red = (double)kYWinWarps * (twojmax + 1) * 2 * 32 * 8;
-    c->y_ta_max = (2.0 * nh * 32 * 8 + red <= 200.0 * 1024) ? 32
-                  : ((2.0 * nh * 16 * 8 + red <= 200.0 * 1024) ? 16 : 8);
     *out = c;
   });
   if (rc != SNAPGPU_OK && c) {
@@ -483,11 +505,9 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   invalidate_graph(c);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  invalidate_csr_graph(c);
   c->d_weights.release();
-  c->d_itw.release();
   c->d_cw.release();
-  c->d_items.release();
-  c->d_rowbeg.release();
 
   c->d_citw[0].release();
   c->d_qunits.release();
@@ -512,8 +532,12 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_etotal.release();
   c->d_out.release();
   if (c->h_out) cudaFreeHost(c->h_out);
-  c->d_part.release();
-  c->d_ticket.release();
+  c->d_epart.release();
+  c->d_tile_sum.release();
+  c->d_tickets.release();
+  c->d_rev_off.release();
+  c->d_rev_cur.release();
+  c->d_rev.release();
   c->d_err.release();
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -626,7 +650,9 @@ int snapgpu_scatter_forces(snapgpu_ctx* c) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_dE, "scatter_forces: no dElist");  // snap_core.hpp:876
-    launch_scatter(c);
+    ensure_csr(c);
+    launch_gather(c);
+    c->have_forces = true;
   });
 }
 
@@ -634,6 +660,7 @@ int snapgpu_run(snapgpu_ctx* c) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_lists, "run: no neighbor lists");
+    ensure_csr(c);
     if (c->timing) {
       run_direct(c);
       CK(cudaEventSynchronize(c->ev[4]));
@@ -661,7 +688,7 @@ int snapgpu_run(snapgpu_ctx* c) {
       }
       CK(cudaGraphLaunch(c->gexec, c->stream));
     }
-    c->have_U = c->have_Y = c->have_dE = true;
+    c->have_U = c->have_Y = c->have_dE = c->have_forces = true;
   });
 }
 
@@ -689,15 +716,18 @@ int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, 
     }
     CK(cudaMemcpyAsync(c->h_out, c->d_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost,
                        c->stream));
+    if (c->ext_forces && forces)
+      CK(cudaMemcpyAsync(forces, c->ext_forces, sizeof(double) * force_doubles(c),
+                         cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (forces) std::memcpy(forces, c->h_out, sizeof(double) * 3 * c->natoms_total);
+    if (forces && !c->ext_forces) std::memcpy(forces, c->h_out, sizeof(double) * force_doubles(c));
     if (eatom && c->nlocal > 0) std::memcpy(eatom, c->h_out + nf, sizeof(double) * c->nlocal);
     if (etotal) *etotal = c->h_out[nf + ne];
     if (*c->h_err) {
       const unsigned f = *c->h_err;
       CK(cudaMemsetAsync(c->d_err.p, 0, sizeof(unsigned), c->stream));
       CK(cudaStreamSynchronize(c->stream));
-      c->have_lists = c->have_U = c->have_Y = c->have_dE = false;
+      c->have_lists = c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
       throw InvalidArg{device_error_message(f)};
     }
   });
@@ -711,9 +741,9 @@ int snapgpu_synchronize(snapgpu_ctx* c) {
 int snapgpu_get_forces(snapgpu_ctx* c, double* f) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    need(c->have_dE, "get_forces before the force pass");
+    need(c->have_forces, "get_forces before scatter_forces");
     require(f != nullptr, "null output");
-    CK(cudaMemcpyAsync(f, c->d_forces.p, sizeof(double) * 3 * c->natoms_total,
+    CK(cudaMemcpyAsync(f, forces_ptr(c), sizeof(double) * force_doubles(c),
                        cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   });
@@ -928,9 +958,9 @@ int snapgpu_get_dedr(snapgpu_ctx* c, double* out) {
 int snapgpu_get_forces_device(snapgpu_ctx* c, double* dst) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    need(c->have_dE, "get_forces_device before the force pass");
+    need(c->have_forces, "get_forces_device before scatter_forces");
     require(dst != nullptr, "null output");
-    CK(cudaMemcpyAsync(dst, c->d_forces.p, sizeof(double) * 3 * c->natoms_total,
+    CK(cudaMemcpyAsync(dst, forces_ptr(c), sizeof(double) * force_doubles(c),
                        cudaMemcpyDeviceToDevice, c->stream));
   });
 }
@@ -978,7 +1008,7 @@ int snapgpu_fp64_peak(int device, int iters, double* tflops, double* ms) {
 int snapgpu_device_outputs(snapgpu_ctx* c, double** forces, double** eatom, double** etotal) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    if (forces) *forces = c->d_forces.p;
+    if (forces) *forces = forces_ptr(c);
     if (eatom) *eatom = c->d_eatom.p;
     if (etotal) *etotal = c->d_etotal.p;
   });
@@ -996,19 +1026,27 @@ int snapgpu_stage_times(snapgpu_ctx* c, float* out4) {
   return SNAPGPU_OK;
 }
 
-int snapgpu_tune(snapgpu_ctx* c, int y_warps, int y_parts, int y_tile_atoms) {
+int snapgpu_tune(snapgpu_ctx* c, int y_parts) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    require(c->y_impl == 0 ? (y_warps == 0 || y_warps == kYWarps)
-                           : (y_warps >= 0 && y_warps <= kYWinWarps),
-            "tune: y_warps must be 12 (2J <= 8) or in [0,12]");
-    require(y_tile_atoms == 0 || y_tile_atoms == 8 || y_tile_atoms == 16 || y_tile_atoms == 32,
-            "tune: y_tile_atoms in {0, 8, 16, 32}");
-    if (y_warps > 0) c->y_warps = y_warps;
+    require(y_parts >= 0 && y_parts <= kMaxYParts, "tune: y_parts must be in [0, 8]");
     c->y_parts = y_parts;
-    c->y_ta_req = y_tile_atoms;
     invalidate_graph(c);
     if (c->have_lists) plan_y(c);
+  });
+}
+
+int snapgpu_set_force_layout(snapgpu_ctx* c, int nchunks, double* ext_forces) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    require(nchunks >= 1 && nchunks <= 256, "set_force_layout: nchunks must be in [1, 256]");
+    CK(cudaStreamSynchronize(c->stream));
+    c->nchunks = nchunks;
+    c->ext_forces = ext_forces;
+    invalidate_graph(c);
+    // re-shape the output buffers on the next list upload
+    c->natoms_total = -1;
+    c->have_lists = c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
   });
 }
 

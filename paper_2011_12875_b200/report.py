@@ -16,10 +16,12 @@ import time
 
 import numpy as np
 
+from .flops import FP64_SPEC_TFLOPS as FP64_PEAK_TFLOPS
+from .flops import step_flops
+
 CSV_HEADER = ("variant,natoms,nnbor,twojmax,steps,wall_ms_per_step,katom_steps_per_s,"
               "speedup_vs_baseline,peak_bytes_total,force_checksum")  # harness.hpp:621-623
 ROOFLINE_COLUMNS = ("step_tflops", "fp64_peak_frac")
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # B200 spec
 
 
 def checksum_hex(x) -> str:
@@ -34,19 +36,6 @@ def checksum_hex(x) -> str:
 
 def _fmt(v: float) -> str:  # detail::fmt_double: shortest round-trip text
     return repr(float(v))
-
-
-def step_flops(twojmax: int, npairs: int, natoms: int) -> float:
-    """Algorithmic FLOPs of one force step (SURVEY.md §8(d) counts)."""
-    import importlib.util
-    import os
-
-    spec = importlib.util.spec_from_file_location(
-        "_bench", os.path.join(os.path.dirname(os.path.dirname(__file__)), "bench.py"))
-    m = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(m)
-    fm = m.flop_model(twojmax)
-    return fm["U_per_pair"] * npairs + fm["Y_per_atom"] * natoms + fm["dE_per_pair"] * npairs
 
 
 def gpu_row(problem, steps: int = 20, baseline_ms: float | None = None, device: int = 0) -> dict:

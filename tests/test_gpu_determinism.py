@@ -1,0 +1,120 @@
+"""Deterministic forces and finite-difference forces on the GPU.
+
+* scatter_forces' deterministic mode (snap_core.hpp:889-899; pipeline.hpp
+  :269-272) walks the pairs serially, F_i += dE(i,k), F_nbr -= dE(i,k).  The
+  engine's force gather pulls the same terms in the same order, so its forces
+  must equal that serialized sum of the engine's own dElist BITWISE, and be
+  bitwise stable run to run and context to context (README.md:111-118: "the
+  force checksum is bitwise stable across runs").
+* finite differences (oracle.hpp:133-172, tests/test_oracle.cpp:137-144):
+  forces are -dE_total/dx by central differences of the GPU total energy,
+  step h = 1e-6 Rcut (tolerances.hpp:32), elementwise rel_err <= 1e-5
+  (tolerances.hpp:41, floor 1e-14 :83), neighbor displacements rebuilt per
+  evaluation keeping the original pairs inside Rcut (oracle.hpp:101-122).
+"""
+import numpy as np
+import pytest
+
+from conftest import fnv1a
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def snap():
+    import paper_2011_12875_b200 as snap
+
+    return snap
+
+
+def serialized_scatter(nbr, numneigh, dedr, natoms):
+    """snap_core.hpp:889-899 in the same floating-point order."""
+    f = np.zeros((natoms, 3))
+    for i in range(numneigh.shape[0]):
+        for k in range(int(numneigh[i])):
+            de = dedr[i, k]
+            j = nbr[i, k]
+            for d in range(3):
+                f[i, d] += de[d]
+                f[j, d] -= de[d]
+    return f
+
+
+@pytest.mark.parametrize("cells,T", [((10, 10, 10), 8), ((3, 3, 3), 14), ((4, 4, 4), 5)])
+def test_forces_are_the_serialized_scatter_of_dedr(snap, cells, T):
+    p = snap.bcc_problem(*cells, twojmax=T)
+    with snap.SnapEngine.for_problem(p) as eng:
+        eng.set_problem(p)
+        eng.run()
+        f = eng.forces()
+        ref = serialized_scatter(p.nbr, p.numneigh, eng.dedr(), p.natoms)
+    assert np.array_equal(f, ref)
+
+
+def test_synthetic_lists_serialized_scatter(snap, port):
+    """Non-symmetric lists (harness.hpp:230-262): the reverse index is general."""
+    p = port.synthetic(64, 14, 8, seed=600)
+    with snap.SnapEngine.for_problem(p) as eng:
+        eng.set_problem(p)
+        eng.compute_U()
+        eng.compute_Y()
+        eng.compute_fused_dE()
+        eng.scatter_forces()
+        f = eng.forces()
+        ref = serialized_scatter(p.nbr, p.numneigh, eng.dedr(), 64)
+    assert np.array_equal(f, ref)
+
+
+def test_forces_bitwise_stable_across_runs_and_contexts(snap):
+    p = snap.bcc_problem(10, 10, 10, twojmax=8)
+    sums = set()
+    for _ in range(2):
+        with snap.SnapEngine.for_problem(p) as eng:
+            eng.set_problem(p)
+            for _ in range(3):
+                eng.run()
+                sums.add(fnv1a(eng.forces()))
+            f, e, t = eng.step(p.numneigh, p.nbr, p.disp)  # one-call path too
+            sums.add(fnv1a(f))
+    assert len(sums) == 1, sums
+
+
+def _lists_from_positions(pos, nbr0, numneigh0, rcut):
+    n = pos.shape[0]
+    S = nbr0.shape[1]
+    nbr = np.zeros((n, S), np.int32)
+    disp = np.zeros((n, S, 3))
+    nn = np.zeros(n, np.int32)
+    for i in range(n):
+        m = 0
+        for k in range(int(numneigh0[i])):
+            j = nbr0[i, k]
+            d = pos[j] - pos[i]
+            if d @ d < rcut * rcut:
+                nbr[i, m] = j
+                disp[i, m] = d
+                m += 1
+        nn[i] = m
+    return nn, nbr, disp
+
+
+@pytest.mark.parametrize("T", [4, 8])
+def test_forces_match_finite_differences(snap, port, T):
+    """tests/test_oracle.cpp:137-144 on the GPU path (make_cluster(8, T, 23+T))."""
+    p = port.make_cluster(8, T, 23 + T)
+    pos = p.positions.copy()
+    h = 1e-6 * p.rcut
+    with snap.SnapEngine.for_problem(p) as eng:
+        f, _, _ = eng.step(p.numneigh, p.nbr, p.disp, p.types)
+        fd = np.zeros_like(f)
+        for i in range(pos.shape[0]):
+            for d in range(3):
+                e = []
+                for s in (+1.0, -1.0):
+                    q = pos.copy()
+                    q[i, d] += s * h
+                    nn, nbr, disp = _lists_from_positions(q, p.nbr, p.numneigh, p.rcut)
+                    e.append(eng.step(nn, nbr, disp, p.types)[2])
+                fd[i, d] = -(e[0] - e[1]) / (2.0 * h)
+    denom = np.maximum(np.maximum(np.abs(f), np.abs(fd)), 1e-14)
+    assert float(np.max(np.abs(f - fd) / denom)) <= 1e-5

@@ -74,12 +74,34 @@ def test_full_size_sampled_atoms_vs_oracle(snap, port, cells, T):
     assert np.abs(f.sum(axis=0)).max() <= 1e-12 * np.abs(f).max() * np.sqrt(n)
     # total energy is the ordered sum of the per-atom energies
     assert abs(etot - float(np.sum(eatom))) <= 1e-12 * abs(etot)
-    # determinism: bitwise equal energies on a second run
+    # determinism: bitwise equal forces and energies on a second run
     eng.run()
     eatom2, etot2 = eng.energy()
     assert etot2 == etot
     assert np.array_equal(eatom2, eatom)
+    assert np.array_equal(eng.forces(), f)
     eng.close()
+
+
+@pytest.mark.parametrize("cells,T", [((64, 64, 32), 8), ((32, 32, 16), 14)],
+                         ids=["C3_2j8_262144", "C4_2j14_32768"])
+def test_full_size_full_vectors_vs_reference(snap, cells, T):
+    """BASELINE.json configs C3 / C4 at full size: the whole force vector,
+    every per-atom energy and the total against the UNMODIFIED reference
+    (oracle/_ref, run_pipeline fused-det on all host threads)."""
+    import os
+
+    import oracle
+
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    p = snap.bcc_problem(*cells, twojmax=T)
+    r = snap.run_pipeline(p)
+    ref = oracle.Ref().run(p, "fused", True, os.cpu_count() or 1,
+                           want=("forces", "eatom", "etotal"))
+    assert normerr(r.forces, ref["forces"]) <= FTOL
+    assert normerr(r.eatom, ref["eatom"]) <= ETOL
+    assert abs(r.etotal - ref["etotal"]) <= ETOL * abs(ref["etotal"])
 
 
 def test_rotation_invariance_bcc2000(snap):
@@ -138,7 +160,7 @@ def test_device_neighbor_lists_bitwise_and_forces(snap, cells, jitter, seed):
     if p.natoms <= 20000:
         eng.run()
         ref = snap.run_pipeline(p)
-        assert normerr(eng.forces(), ref.forces) <= 1e-13  # same lists; scatter order varies
+        assert np.array_equal(eng.forces(), ref.forces)  # same lists: bitwise
         assert eng.energy()[1] == ref.etotal
     eng.close()
 

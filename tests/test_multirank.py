@@ -1,8 +1,8 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): slab partition,
-partial-force scatter, force reduce-scatter and energy all-reduce give the
-single-process result.  The per-rank compute is the oracle
-(dE per pair); the GPU kernels' partition path is covered by
-tests/test_gpu_parity.py::test_partition_sum_equals_full."""
+"""Multi-rank host logic on CPU (gloo, world_size 2): slab partition, the
+chunked partial-force layout with its energy slots, and the single
+reduce-scatter give the single-process forces and total energy (SURVEY.md
+§8(e)).  The per-rank compute is the oracle (dE per pair); the engine's
+partition path runs in tests/test_gpu_multirank.py (two ranks on one GPU)."""
 import os
 import socket
 
@@ -29,36 +29,35 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import oracle
-        import paper_2011_12875_b200 as snap
 
         port_ = oracle.Port()
-        p = snap.bcc_problem(4, 4, 3 * world, twojmax=4)
+        p = port_.bcc_problem(4, 4, 3 * world, 4)
         ref = port_.run(p, want=("forces", "eatom", "etotal", "delist"))
-        n = p.natoms
+        n = p.numneigh.shape[0]
         lo, hi = D.slab_bounds(n, world, rank)
-        part = D.partial_forces_host(p.nbr[lo:hi], p.numneigh[lo:hi], ref["delist"][lo:hi], lo, n)
-        rows = D.padded_rows(n, world)
-        buf = torch.zeros(rows * 3, dtype=torch.float64)
-        buf[: n * 3] = torch.from_numpy(part.reshape(-1))
-        own = D.reduce_forces(buf, world, rank, n).numpy().reshape(-1, 3)
-        k = rows // world
-        glo = np.arange(rank * k, min((rank + 1) * k, n))
-        ferr = np.abs(own[: len(glo)] - ref["forces"][glo]).max() / np.abs(ref["forces"]).max()
-        e = torch.tensor([ref["eatom"][lo:hi].sum()], dtype=torch.float64)
-        D.reduce_energy(e)
-        eerr = abs(float(e[0]) - ref["etotal"]) / abs(ref["etotal"])
+        e_own = float(ref["eatom"][lo:hi].sum())
+        part = D.chunked_partial_host(p.nbr[lo:hi], p.numneigh[lo:hi], ref["delist"][lo:hi],
+                                      lo, n, world, e_own)
+        chunk = D.reduce_chunks(torch.from_numpy(part), world, rank).numpy()
+        k = D.chunk_rows(n, world)
+        own = chunk[: 3 * (hi - lo)].reshape(-1, 3)
+        ferr = np.abs(own - ref["forces"][lo:hi]).max() / np.abs(ref["forces"]).max()
+        eerr = abs(float(chunk[3 * k]) - ref["etotal"]) / abs(ref["etotal"])
         q.put((rank, ferr, eerr, lo, hi))
     finally:
         dist.destroy_process_group()
 
 
 def test_slab_bounds_cover_all_atoms():
-    for n, w in [(2000, 1), (2000, 2), (2001, 4), (16000, 8), (7, 3)]:
+    for n, w in [(2000, 1), (2000, 2), (2001, 4), (16000, 8), (7, 3), (10, 4)]:
         got = [D.slab_bounds(n, w, r) for r in range(w)]
         assert got[0][0] == 0 and got[-1][1] == n
         assert all(a[1] == b[0] for a, b in zip(got[:-1], got[1:]))
-        assert max(h - l for l, h in got) - min(h - l for l, h in got) <= 1
-        assert D.padded_rows(n, w) % w == 0 and D.padded_rows(n, w) >= n
+        k = D.chunk_rows(n, w)
+        # the owned slab of rank r is exactly the atoms of force chunk r
+        assert all(lo == min(n, r * k) and hi == min(n, (r + 1) * k)
+                   for r, (lo, hi) in enumerate(got))
+        assert D.chunk_stride(n, w) == 3 * k + 1
 
 
 @pytest.mark.parametrize("world", [2])

@@ -29,5 +29,5 @@ def run(nx, ny, nz, T=8, reps=10, tune=None):
 if __name__ == "__main__":
     for spec in sys.argv[1:]:
         f = [int(x) for x in spec.split(",")]
-        tune = tuple(f[4:7]) if len(f) > 4 else None
+        tune = (f[4],) if len(f) > 4 else None
         run(f[0], f[1], f[2], T=f[3], reps=10 if f[0]*f[1]*f[2] < 50000 else 3, tune=tune)

@@ -10,7 +10,7 @@ T = 8
 p = snap.bcc_problem(nx, ny, nz, twojmax=T)
 eng = snap.SnapEngine.for_problem(p)
 eng.set_problem(p)
-if parts: eng.tune(0, parts, 0)
+if parts: eng.tune(parts)
 eng.enable_stage_timing(True)  # direct launches (the profile buffer is allocated lazily)
 eng.run(); eng.synchronize()
 L = snap.library()
