@@ -1668,20 +1668,24 @@ struct GatherArgs {
   const double* etotal;  // this rank's total (nchunks > 1)
 };
 
-// One warp per atom: the lanes fetch 32 terms of the atom's merged sequence
-// at a time (reverse slots before its own row, its own row, the remaining
-// reverse slots) with independent loads, then every lane adds them in
-// sequence order (the serialized order of snap_core.hpp:889-899; a - x and
-// a + (-x) round identically).
-__global__ void __launch_bounds__(256) k_gather_forces(const GatherArgs A) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (A.nchunks > 1 && blockIdx.x == 0 && threadIdx.x < A.nchunks)
-    A.forces[(size_t)threadIdx.x * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
-  const int a = gw;
+// One thread per (atom, component).  Up to kGatherCap reverse slots and own
+// pairs are fetched with independent (unrolled, predicated) loads, then added
+// in the serialized order of snap_core.hpp:889-899: the reverse slots of
+// earlier rows, the atom's own row, the reverse slots of later rows
+// (a - x and a + (-x) round identically).  Longer lists fall back to a
+// serial walk in the same order.
+constexpr int kGatherCap = 32;
+
+__global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (A.nchunks > 1 && t < A.nchunks)
+    A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
+  const int a = t / 3, d = t - 3 * (t / 3);
   if (a >= A.pr.natoms_total) return;
-  double* fo = A.forces + (size_t)(a / A.chunk_rows) * A.chunk_stride + (size_t)(a % A.chunk_rows) * 3;
+  double* fo = A.forces + (size_t)(a / A.chunk_rows) * A.chunk_stride +
+               (size_t)(a % A.chunk_rows) * 3 + d;
   if (pipeline_failed(A.pr)) {
-    if (lane < 3) fo[lane] = 0.0;
+    *fo = 0.0;
     return;
   }
   const int S = A.pr.stride;
@@ -1693,46 +1697,38 @@ __global__ void __launch_bounds__(256) k_gather_forces(const GatherArgs A) {
     nn = A.pr.numneigh[il];
     nn = (nn < 0 || nn > S) ? 0 : nn;
   }
-  // reverse slots that precede the own row (the slots are sorted)
-  int nbefore = 0;
-  if (nn > 0)
-    for (int b = 0; b < nrev; b += 32) {
-      const bool lt = (b + lane < nrev) && (A.rev[s0 + b + lane] < own);
-      nbefore += __popc(__ballot_sync(0xffffffffu, lt));
+  double f = 0.0;
+  if (nrev <= kGatherCap && nn <= kGatherCap) {
+    int p[kGatherCap];
+    double v[kGatherCap], w[kGatherCap];
+#pragma unroll
+    for (int q = 0; q < kGatherCap; ++q) p[q] = q < nrev ? __ldg(A.rev + s0 + q) : 0;
+#pragma unroll
+    for (int q = 0; q < kGatherCap; ++q) w[q] = q < nn ? A.dedr[(size_t)(own + q) * 3 + d] : 0.0;
+    int nb = 0;
+#pragma unroll
+    for (int q = 0; q < kGatherCap; ++q) {
+      v[q] = q < nrev ? A.dedr[(size_t)p[q] * 3 + d] : 0.0;
+      nb += (q < nrev && p[q] < own) ? 1 : 0;
     }
-  const int M = nrev + nn;
-  double fx = 0.0, fy = 0.0, fz = 0.0;
-  for (int b = 0; b < M; b += 32) {
-    const int q = b + lane;
-    double vx = 0.0, vy = 0.0, vz = 0.0;
-    if (q < M) {
-      int p;
-      double sg = -1.0;
-      if (q < nbefore) {
-        p = A.rev[s0 + q];
-      } else if (q < nbefore + nn) {
-        p = own + (q - nbefore);
-        sg = 1.0;
-      } else {
-        p = A.rev[s0 + q - nn];
-      }
-      const double* de = A.dedr + (size_t)p * 3;
-      vx = sg * de[0];
-      vy = sg * de[1];
-      vz = sg * de[2];
-    }
-    const int cnt = min(32, M - b);
-    for (int t = 0; t < cnt; ++t) {
-      fx += __shfl_sync(0xffffffffu, vx, t);
-      fy += __shfl_sync(0xffffffffu, vy, t);
-      fz += __shfl_sync(0xffffffffu, vz, t);
-    }
+#pragma unroll
+    for (int q = 0; q < kGatherCap; ++q)
+      if (q < nb) f -= v[q];
+#pragma unroll
+    for (int q = 0; q < kGatherCap; ++q)
+      if (q < nn) f += w[q];
+#pragma unroll
+    for (int q = 0; q < kGatherCap; ++q)
+      if (q >= nb && q < nrev) f -= v[q];
+  } else {
+    int s = s0;
+    const int e = s0 + nrev;
+    if (nn > 0)
+      for (; s < e && A.rev[s] < own; ++s) f -= A.dedr[(size_t)A.rev[s] * 3 + d];
+    for (int k = 0; k < nn; ++k) f += A.dedr[(size_t)(own + k) * 3 + d];
+    for (; s < e; ++s) f -= A.dedr[(size_t)A.rev[s] * 3 + d];
   }
-  if (lane == 0) {
-    fo[0] = fx;
-    fo[1] = fy;
-    fo[2] = fz;
-  }
+  *fo = f;
 }
 
 // ===========================================================================

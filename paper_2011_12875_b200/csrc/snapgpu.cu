@@ -243,8 +243,9 @@ void launch_gather(snapgpu_ctx* c) {
   a.chunk_stride = c->chunk_stride();
   a.nchunks = c->nchunks;
   a.etotal = c->d_etotal.p;
-  if (c->natoms_total > 0) {  // one warp per atom
-    k_gather_forces<<<(c->natoms_total + 7) / 8, 256, 0, c->stream>>>(a);
+  const int nthr = std::max(3 * c->natoms_total, c->nchunks);
+  if (c->natoms_total > 0) {  // one thread per force component
+    k_gather_forces<<<(nthr + 127) / 128, 128, 0, c->stream>>>(a);
     CK(cudaGetLastError());
   }
 }
