@@ -147,10 +147,11 @@ int snapgpu_set_positions(snapgpu_ctx* ctx, int natoms, const double* pos,
 int snapgpu_get_neighbors(snapgpu_ctx* ctx, int* numneigh, int* nbr, double* disp);
 
 /* Bispectrum descriptors B_l(i) (compute_B_from_U,
- * snap_core.hpp:642-681) of the owned atoms, blist[i * ntriples + l], via the
- * energy identity E_i = sum_l beta_l B_l(i) (compute_energy :684-701):
- * compute_Y once per triple with one-hot beta (a fitting / validation path,
- * ntriples compute_Y launches).  beta is restored; rerun the force step. */
+ * snap_core.hpp:642-681, b_contract :556-575) of the owned atoms,
+ * blist[i * ntriples + l], in one pass over Ulisttot (k_compute_B: every
+ * canonical triple's coupling elements formed on the fly and contracted,
+ * never stored).  Runs compute_U first if needed; Y', dElist and forces are
+ * untouched. */
 int snapgpu_compute_descriptors(snapgpu_ctx* ctx, double* blist);
 
 /* Virial of the owned pairs from dElist (the paper keeps

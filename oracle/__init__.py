@@ -261,6 +261,9 @@ class Ref:
         L.ref_generate_synthetic.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double,
                                              C.c_uint64, _ip, _ip, _dp, _dp]
         L.ref_oracle_checks.argtypes = self._PROB + [C.c_uint64, _dp]
+        L.ref_save_problem.argtypes = self._PROB + [C.c_uint64, C.c_int, C.c_double,
+                                                    C.c_void_p, C.c_char_p]
+        L.ref_resave_problem.argtypes = [C.c_char_p, C.c_char_p]
 
     def err(self):
         return self.L.ref_last_error().decode()
@@ -380,6 +383,20 @@ class Ref:
                                self_flag=1, beta=beta, weights=np.ones(1), types=None,
                                numneigh=numneigh, nbr=nbr.reshape(natoms, nnbor),
                                disp=disp.reshape(natoms, nnbor, 3))
+
+    def save_problem(self, p, path, seed=0, synthetic=False, box_length=0.0):
+        """harness::save_problem (harness.hpp:770-775) of problem p."""
+        d = _arrays(p)
+        pos = getattr(p, "positions", None)
+        pos = None if pos is None else np.ascontiguousarray(pos, np.float64)
+        if self.L.ref_save_problem(*self._pargs(p, d), int(seed), int(bool(synthetic)),
+                                   float(box_length), _ptr(pos), str(path).encode()):
+            raise ValueError(self.err())
+
+    def resave_problem(self, in_path, out_path):
+        """harness::load_problem (validating) then harness::save_problem."""
+        if self.L.ref_resave_problem(str(in_path).encode(), str(out_path).encode()):
+            raise ValueError(self.err())
 
     def oracle_checks(self, p, seed=77):
         d = _arrays(p)

@@ -332,4 +332,32 @@ int ref_oracle_checks(int twojmax, double rcut, double rmin0, double rfac0,
   });
 }
 
+// Problem file I/O through the reference's own writer / reader
+// (harness.hpp:698-780, schema 1, shortest round-trip doubles):
+// ref_save_problem writes the given problem (positions may be NULL);
+// ref_resave_problem loads a file with harness::load_problem (which runs
+// Problem::validate) and writes it back with harness::save_problem.
+int ref_save_problem(int twojmax, double rcut, double rmin0, double rfac0, double wself,
+                     int self_flag, const double* beta, int nbeta, const double* weights,
+                     int nweights, int natoms, int stride, const int* numneigh,
+                     const int* nbr, const double* disp, const int* types,
+                     std::uint64_t seed, int synthetic, double box_length,
+                     const double* positions, const char* path) {
+  return guarded([&] {
+    Problem p = make_problem(twojmax, rcut, rmin0, rfac0, wself, self_flag, beta, nbeta,
+                             weights, nweights, natoms, stride, numneigh, nbr, disp, types);
+    p.seed = seed;
+    p.synthetic = synthetic != 0;
+    p.box_length = box_length;
+    if (positions)
+      for (int i = 0; i < natoms; ++i)
+        p.positions.push_back({positions[3 * i], positions[3 * i + 1], positions[3 * i + 2]});
+    harness::save_problem(p, path);
+  });
+}
+
+int ref_resave_problem(const char* in_path, const char* out_path) {
+  return guarded([&] { harness::save_problem(harness::load_problem(in_path), out_path); });
+}
+
 }  // extern "C"

@@ -149,6 +149,9 @@ class Problem:
     types: Optional[np.ndarray] = None
     positions: Optional[np.ndarray] = None
     box: Optional[np.ndarray] = None
+    seed: int = 0             # Problem::seed (snap_core.hpp:70)
+    synthetic: bool = False   # Problem::synthetic (:71)
+    box_length: float = 0.0   # Problem::box_length (:69): cubic edge, 0 if not periodic
 
     @property
     def natoms(self) -> int:
@@ -169,10 +172,45 @@ class Problem:
             return p
         kw = {k: getattr(p, k) for k in ("twojmax", "rcut", "rmin0", "rfac0", "wself",
                                           "self_flag", "beta", "numneigh", "nbr", "disp")}
-        for k in ("weights", "types", "positions", "box"):
+        for k in ("weights", "types", "positions", "box", "seed", "synthetic", "box_length"):
             if getattr(p, k, None) is not None:
                 kw[k] = getattr(p, k)
         return cls(**kw)
+
+    def validate(self) -> "Problem":
+        """Problem::validate (snap_core.hpp:89-118) on the host arrays."""
+        n = self.natoms
+        nb = counts(self.twojmax)["n_triples"]
+        if not (self.rcut > self.rmin0):
+            raise InvalidArgument("problem: Rcut must exceed rmin0")
+        if np.asarray(self.beta).size != nb:
+            raise InvalidArgument("problem: beta length must match the triple count")
+        w = np.asarray(self.weights)
+        if w.size == 0:
+            raise InvalidArgument("problem: empty weight table")
+        if self.types is not None:
+            t = np.asarray(self.types)
+            if t.size != n or (n and (t.min() < 0 or t.max() >= w.size)):
+                raise InvalidArgument("problem: atom type outside weight table")
+        if self.positions is not None and np.asarray(self.positions).shape[0] not in (0, n):
+            raise InvalidArgument("problem: positions/neighbors size mismatch")
+        nn = np.asarray(self.numneigh)
+        S = self.stride
+        if n and (nn.min() < 0 or nn.max() > S):
+            raise InvalidArgument("problem: neighbor count outside stride")
+        mask = np.arange(S)[None, :] < nn[:, None]
+        nbr = np.asarray(self.nbr).reshape(n, S)
+        disp = np.asarray(self.disp).reshape(n, S, 3)
+        if np.any(mask & ((nbr < 0) | (nbr >= n))):
+            raise InvalidArgument("problem: neighbor index out of range")
+        if np.any(mask & (nbr == np.arange(n)[:, None])):
+            raise InvalidArgument("problem: self neighbor")
+        r2 = (disp * disp).sum(-1)
+        if np.any(mask & ~(r2 > 0.0)):
+            raise InvalidArgument("problem: zero-length neighbor displacement")
+        if np.any(mask & ~(r2 < self.rcut * self.rcut)):
+            raise InvalidArgument("problem: neighbor at or beyond Rcut")
+        return self
 
 
 @dataclass
@@ -487,4 +525,5 @@ def bcc_problem(nx, ny, nz, twojmax=8, seed=2011, a=3.1803, jitter=0.05, rcut=4.
     box = np.array([nx * a, ny * a, nz * a])
     numneigh, nbr, disp = build_neighborlist(pos, box, rcut)
     return Problem(twojmax=int(twojmax), rcut=float(rcut), beta=beta, numneigh=numneigh,
-                   nbr=nbr, disp=disp, positions=pos, box=box)
+                   nbr=nbr, disp=disp, positions=pos, box=box, seed=int(seed),
+                   box_length=float(box[0]) if nx == ny == nz else 0.0)

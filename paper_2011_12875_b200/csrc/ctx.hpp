@@ -119,6 +119,11 @@ struct snapgpu_ctx {
   double* h_out = nullptr;                 // pinned staging of d_out (one-call API)
   size_t h_out_n = 0;
 
+  // direct bispectrum components (kernels.cuh k_compute_B), built on first use
+  snapgpu::host::DevBuf<int4> d_bitems;
+  snapgpu::host::DevBuf<int> d_bcwoff, d_btbeg;
+  snapgpu::host::DevBuf<double> d_bwgt, d_blist;
+
   // deterministic energy epilogue (kernels.cuh energy_epilogue)
   snapgpu::host::DevBuf<double> d_epart, d_tile_sum;
   snapgpu::host::DevBuf<unsigned> d_tickets;  // [0]: global ticket, [1..]: per tile
@@ -185,6 +190,7 @@ inline EnergyOut energy_out(snapgpu_ctx* c) {
 template <int T> void launch_U_t(snapgpu_ctx* c);
 template <int T> void launch_Y_t(snapgpu_ctx* c);
 template <int T> void launch_DE_t(snapgpu_ctx* c);
+template <int T> void launch_B_t(snapgpu_ctx* c, double* blist);
 struct YTablesHost {  // constant-bank tables of k_compute_Y_cwin (kernels.cuh)
   std::vector<double> cw;
   std::vector<uint4> items4, items12;

@@ -953,6 +953,93 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs
 }
 
 // ===========================================================================
+// Bispectrum components B_l(i) straight from V (compute_B_from_U,
+// snap_core.hpp:642-681 with b_contract :556-575): one pass, every triple.
+// CTA = a tile of TA atoms (32 for 2J <= 8, 8 above) with its full mirrored
+// stack X in shared memory (the compute_Y staging), 12 warps; warp w takes
+// triples w, w+12, ...; lane = (item slot s, atom a): the slots split the
+// triple's items (rows mb <= j/2, all mb1), each item contracted at once:
+//     B += w' W_B sum_ma Re( [sum_a2 C'(ma+D-a2, a2) x1[ma+D-a2] x2[a2]] conj V(j,mb,ma) )
+// (v-space: the bracket is Z_u / f and V = f U, so the product is Z_u U*).
+// The slots are combined by xor-shuffles in a fixed order: deterministic.
+// A descriptor / fitting path, not the force step.
+// ===========================================================================
+struct BArgs {
+  const double* V;
+  const int* expand;     // half -> full scatter map
+  const int4* items;     // b_plan items
+  const int* cwoff;      // per item: windowed C' block
+  const double* wgt;     // per item: w' W_B
+  const int* tbeg;       // per triple: first item, + end
+  const double* cw;      // windowed C' (y_plan layout)
+  int ntriples, nlocal;
+  double* blist;         // [atom][ntriples]
+};
+
+template <int T>
+__global__ void __launch_bounds__(384, 1) k_compute_B(const BArgs A) {
+  constexpr int TA = T <= 8 ? 32 : 8;   // atoms per CTA
+  constexpr int SUB = 32 / TA;          // item slots per warp
+  constexpr int PAD = 16;
+  constexpr int NF = c_full_off(T + 1);
+  constexpr int NP = NF + 2 * PAD;
+  constexpr int NH = c_half_off(T + 1);
+  extern __shared__ double smem[];
+  double* sX = smem;  // [re|im][pad | full idx | pad][TA]
+  const int atom0 = blockIdx.x * TA;
+  for (int e = threadIdx.x; e < PAD * TA; e += blockDim.x) {
+    sX[e] = sX[(PAD + NF) * TA + e] = 0.0;
+    sX[NP * TA + e] = sX[(NP + PAD + NF) * TA + e] = 0.0;
+  }
+  const double* Vt = A.V + (size_t)(atom0 >> 5) * 2 * NH * 32 + (atom0 & 31);
+  for (int e = threadIdx.x; e < NH * TA; e += blockDim.x) {
+    const int h = e / TA, a = e - h * TA;
+    const double re = __ldg(Vt + h * 32 + a), im = __ldg(Vt + (NH + h) * 32 + a);
+    const int2 sc = __ldg(reinterpret_cast<const int2*>(A.expand) + h);
+    sX[(PAD + sc.x) * TA + a] = re;
+    sX[(NP + PAD + sc.x) * TA + a] = im;
+    if (sc.y >= 0) {
+      const int fm = sc.y >> 1;
+      const bool neg = sc.y & 1;
+      sX[(PAD + fm) * TA + a] = neg ? -re : re;
+      sX[(NP + PAD + fm) * TA + a] = neg ? im : -im;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int a = lane % TA, sl = lane / TA;
+  const int atom = atom0 + a;
+  for (int l = w; l < A.ntriples; l += nw) {
+    double b = 0.0;
+    const int i1 = __ldg(A.tbeg + l + 1);
+    for (int it = __ldg(A.tbeg + l) + sl; it < i1; it += SUB) {
+      const int4 m = __ldg(A.items + it);
+      const int J2 = m.w & 0xff, J = m.w >> 8;
+      const double* c0 = A.cw + __ldg(A.cwoff + it);
+      const double* x1 = sX + (PAD + m.x) * TA + a;  // x1[D + k] at x1[k * TA]
+      const double* x2 = sX + (PAD + m.y) * TA + a;
+      const double* xr = sX + (PAD + m.z) * TA + a;
+      double part = 0.0;
+      for (int ma = 0; ma <= J; ++ma) {
+        double zr = 0.0, zi = 0.0;
+        for (int a2 = 0; a2 <= J2; ++a2) {
+          const double cc = __ldg(c0 + a2 * (J + 1) + ma);
+          const double ur = x1[(ma - a2) * TA], ui = x1[(NP + ma - a2) * TA];
+          const double vr = x2[a2 * TA], vi = x2[(NP + a2) * TA];
+          zr = fma(cc, ur * vr - ui * vi, zr);
+          zi = fma(cc, ur * vi + ui * vr, zi);
+        }
+        part += zr * xr[ma * TA] + zi * xr[(NP + ma) * TA];
+      }
+      b = fma(__ldg(A.wgt + it), part, b);
+    }
+#pragma unroll
+    for (int o = TA; o < 32; o <<= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (sl == 0 && atom < A.nlocal) A.blist[(size_t)atom * A.ntriples + l] = b;
+  }
+}
+
+// ===========================================================================
 // compute_Y, constant-window cooperative variant (2J <= 8)
 //
 // CTA = one 32-atom tile (lane = atom), its FULL mirrored stack X in shared

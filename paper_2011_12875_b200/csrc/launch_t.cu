@@ -145,6 +145,28 @@ void launch_Y_t(snapgpu_ctx* c) {
 }
 
 template <int T>
+void launch_B_t(snapgpu_ctx* c, double* blist) {
+  constexpr int TA = T <= 8 ? 32 : 8;
+  constexpr int NP = c_full_off(T + 1) + 2 * 16;
+  BArgs a;
+  a.V = c->d_V.p;
+  a.expand = c->d_expand.p;
+  a.items = c->d_bitems.p;
+  a.cwoff = c->d_bcwoff.p;
+  a.wgt = c->d_bwgt.p;
+  a.tbeg = c->d_btbeg.p;
+  a.cw = c->d_cw.p;
+  a.ntriples = static_cast<int>(c->maps.triples.size());
+  a.nlocal = c->nlocal;
+  a.blist = blist;
+  const size_t smem = sizeof(double) * 2 * NP * TA;
+  CK(cudaFuncSetAttribute(k_compute_B<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  k_compute_B<T><<<(c->nlocal + TA - 1) / TA, 384, smem, c->stream>>>(a);
+  CK(cudaGetLastError());
+}
+
+template <int T>
 void launch_DE_t(snapgpu_ctx* c) {
   using R = DERCfg<T>;
   DEArgs a;
@@ -197,6 +219,7 @@ void upload_ytables_t(int device, const YTablesHost& t) {
 template void launch_U_t<SNAP_T>(snapgpu_ctx*);
 template void launch_Y_t<SNAP_T>(snapgpu_ctx*);
 template void launch_DE_t<SNAP_T>(snapgpu_ctx*);
+template void launch_B_t<SNAP_T>(snapgpu_ctx*, double*);
 template void upload_ytables_t<SNAP_T>(int, const YTablesHost&);
 
 }  // namespace host

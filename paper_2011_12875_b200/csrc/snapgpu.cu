@@ -533,6 +533,11 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_etotal.release();
   c->d_out.release();
   if (c->h_out) cudaFreeHost(c->h_out);
+  c->d_bitems.release();
+  c->d_bcwoff.release();
+  c->d_btbeg.release();
+  c->d_bwgt.release();
+  c->d_blist.release();
   c->d_epart.release();
   c->d_tile_sum.release();
   c->d_tickets.release();
@@ -562,36 +567,38 @@ int snapgpu_compute_descriptors(snapgpu_ctx* c, double* blist) {
   if (!c || !blist) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_lists, "compute_descriptors: no neighbor lists");
-    // B_l(i) through the energy identity E_i = sum_l beta_l B_l(i)
-    // (compute_energy, snap_core.hpp:684-701): compute_Y with one-hot beta
-    // per triple gives E_i = B_l(i) (compute_B_from_U, :642-681)
-    if (!c->have_U) launch_U(c);
-    const int nt = static_cast<int>(c->maps.triples.size());
-    const int n = c->nlocal;
-    const std::vector<double> saved = c->beta;
-    std::vector<double> col(std::max(1, n));
-    try {
-      for (int l = 0; l < nt; ++l) {
-        CK(cudaStreamSynchronize(c->stream));
-        c->beta.assign(nt, 0.0);
-        c->beta[l] = 1.0;
-        upload_beta(c);
-        launch_Y(c);
-        if (n > 0)
-          CK(cudaMemcpyAsync(col.data(), c->d_eatom.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                             c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        for (int i = 0; i < n; ++i) blist[(size_t)i * nt + l] = col[i];
-      }
-    } catch (...) {
-      c->beta = saved;
-      upload_beta(c);
-      throw;
+    // B_l(i) (compute_B_from_U, snap_core.hpp:642-681) in one pass over V
+    if (!c->d_bitems.p) {
+      const BPlan bp = b_plan(c->maps, c->cg);
+      std::vector<int4> it(bp.items.size());
+      for (size_t q = 0; q < it.size(); ++q)
+        it[q] = make_int4(bp.items[q][0], bp.items[q][1], bp.items[q][2], bp.items[q][3]);
+      auto up = [](auto& buf, const auto& v) {
+        using E = typename std::decay_t<decltype(v)>::value_type;
+        buf.alloc(std::max<size_t>(1, v.size()));
+        CK(cudaMemcpy(buf.p, v.data(), v.size() * sizeof(E), cudaMemcpyHostToDevice));
+      };
+      up(c->d_bitems, it);
+      up(c->d_bcwoff, bp.cwoff);
+      up(c->d_bwgt, bp.wgt);
+      up(c->d_btbeg, bp.triple_begin);
+      if (!c->d_cw.p) up(c->d_cw, c->yplan.cw);
     }
-    c->beta = saved;
-    upload_beta(c);
+    if (!c->have_U) launch_U(c);
     c->have_U = true;
-    c->have_Y = c->have_dE = false;  // Y' and the energies belong to the one-hot runs
+    const size_t nb = (size_t)std::max(1, c->nlocal) * c->maps.triples.size();
+    c->d_blist.alloc(nb);
+    if (c->nlocal > 0) {
+      using Fn = void (*)(snapgpu_ctx*, double*);
+      pick_T<Fn>(c->T, launch_B_t<0>, launch_B_t<1>, launch_B_t<2>, launch_B_t<3>,
+                 launch_B_t<4>, launch_B_t<5>, launch_B_t<6>, launch_B_t<7>, launch_B_t<8>,
+                 launch_B_t<9>, launch_B_t<10>, launch_B_t<11>, launch_B_t<12>, launch_B_t<13>,
+                 launch_B_t<14>)(c, c->d_blist.p);
+      CK(cudaMemcpyAsync(blist, c->d_blist.p,
+                         sizeof(double) * (size_t)c->nlocal * c->maps.triples.size(),
+                         cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

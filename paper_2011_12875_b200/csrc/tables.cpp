@@ -465,6 +465,43 @@ std::vector<double> ycoop_weights(const YCoopPlan& p, const IndexMaps& m,
   return out;
 }
 
+BPlan b_plan(const IndexMaps& m, const std::vector<double>& cg) {
+  BPlan p;
+  std::vector<int> cwoff(m.tuples.size());
+  int o = 0;
+  for (std::size_t q = 0; q < m.tuples.size(); ++q) {  // y_plan's windowed C' layout
+    cwoff[q] = o;
+    o += (m.tuples[q].j2 + 1) * (m.tuples[q].j + 1);
+  }
+  auto G = [](int t, int mm) { return g_scale(t, std::min(mm, t - mm)); };
+  for (const auto& tr : m.triples) {
+    p.triple_begin.push_back(static_cast<int>(p.items.size()));
+    const int j1 = tr[0], j2 = tr[1], j = tr[2];
+    int q = -1;
+    for (std::size_t k = 0; k < m.tuples.size(); ++k)
+      if (m.tuples[k].j1 == j1 && m.tuples[k].j2 == j2 && m.tuples[k].j == j) q = static_cast<int>(k);
+    const Tuple& tp = m.tuples[q];
+    const int D = (j1 + j2 - j) / 2;
+    for (int mb = 0; 2 * mb <= j; ++mb) {
+      const double wrow = (2 * mb < j) ? 2.0 : 1.0;
+      const int lo = std::max(0, mb + D - j2), hi = std::min(j1, mb + D);
+      for (int mb1 = lo; mb1 <= hi; ++mb1) {
+        const int mb2 = mb + D - mb1;
+        const int x1 = m.full_off[j1] + mb1 * (j1 + 1) + D;
+        const int x2 = m.full_off[j2] + mb2 * (j2 + 1);
+        const int xr = m.full_off[j] + mb * (j + 1);
+        p.items.push_back({x1, x2, xr, j2 | (j << 8)});
+        p.cwoff.push_back(cwoff[q]);
+        const double wb = cg[tp.cg_off + mb1 * (j2 + 1) + mb2] /
+                          (G(j1, mb1) * G(j2, mb2) * g_scale(j, mb));
+        p.wgt.push_back(wrow * wb);
+      }
+    }
+  }
+  p.triple_begin.push_back(static_cast<int>(p.items.size()));
+  return p;
+}
+
 std::vector<int> y_row_schedule(const IndexMaps& m, const std::vector<double>& row_cost,
                                 int workers, int* cap) {
   std::vector<std::pair<double, int>> items;

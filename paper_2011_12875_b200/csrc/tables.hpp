@@ -121,6 +121,22 @@ YQuadPlan yquad_plan(const IndexMaps& m, int warps, int groups);
 std::vector<double> yquad_weights(const YQuadPlan& p, const IndexMaps& m,
                                   const std::vector<double>& wtab);
 
+// Direct bispectrum components B_l (compute_B_from_U, snap_core.hpp:642-681;
+// kernels.cuh k_compute_B).  Per canonical triple l = tuple (j1, j2, j):
+// items {x1 window base (full idx + D), x2 row base (full idx), (j, mb) row
+// base (full idx), j2 | j << 8}, the C' block offset (y_plan windowed
+// layout) and the weight w' W_B(mb1, mb2), with W_B the beta-free W table
+// (w_table with every folded beta = 1) and w' = 2 on strict rows, 1 on the
+// middle row (b_contract, snap_core.hpp:556-575: the middle row runs over all
+// ma).  triple_begin[l] .. [l+1]: the triple's items.
+struct BPlan {
+  std::vector<std::array<int, 4>> items;
+  std::vector<int> cwoff;
+  std::vector<double> wgt;
+  std::vector<int> triple_begin;
+};
+BPlan b_plan(const IndexMaps& m, const std::vector<double>& cg);
+
 // LPT assignment of rows to workers: [worker][cap] row codes j*64+mb, -1 end.
 std::vector<int> y_row_schedule(const IndexMaps& m, const std::vector<double>& row_cost,
                                 int workers, int* cap);

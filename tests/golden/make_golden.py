@@ -90,6 +90,14 @@ def main():
     save("synthetic_n64_k14_2j8_s600", s6, R.run(s6, "v1", True, 4, LIGHT),
          extra={"fnv_checksum": np.array("dd6d6cc7a1c2e358")})
 
+    # Problem files written by the reference's own save_problem
+    # (harness.hpp:698-780, schema 1): the BCC lattice with positions and
+    # its cubic box, and a typed ragged cluster.
+    R.save_problem(bcc, os.path.join(HERE, "bcc54_2j8.problem.json"), seed=2011,
+                   box_length=float(box[0]))
+    c7 = R.make_cluster(7, 5, 915, 3)
+    R.save_problem(c7, os.path.join(HERE, "cluster_n7_2j5_s915_t3.problem.json"), seed=915)
+
     # Known-answer tables.
     tabs = {}
     for T in (0, 2, 4, 8, 14):

@@ -167,11 +167,12 @@ def test_device_neighbor_lists_bitwise_and_forces(snap, cells, jitter, seed):
 
 def test_descriptors_vs_oracle_blist(snap, port):
     """B_l(i) (compute_B_from_U, snap_core.hpp:642-681) from
-    one-hot-beta compute_Y runs equals the oracle's blist; the force step is
-    unchanged afterwards (beta restored)."""
+    the one-pass k_compute_B equals the oracle's blist at 2J = 4, 5, 8, 14
+    (typed clusters included) and satisfies E_i = sum_l beta_l B_l."""
     from conftest import load_golden
 
-    for name in ("cluster_n6_2j8_s910_t1", "bcc54_2j8", "cluster_n5_2j4_s906_t1"):
+    for name in ("cluster_n6_2j8_s910_t1", "bcc54_2j8", "cluster_n5_2j4_s906_t1",
+                 "bcc54_2j14", "cluster_n7_2j5_s915_t3", "cluster_n4_2j14_s914_t1"):
         p, out, _ = load_golden(name)
         pr = snap.Problem.from_any(p)
         eng = snap.SnapEngine.for_problem(pr)
@@ -179,7 +180,11 @@ def test_descriptors_vs_oracle_blist(snap, port):
         b = eng.descriptors()
         ref = port.run(pr, want=("blist",))["blist"]
         assert normerr(b, ref) <= 1e-11, name
+        assert np.array_equal(eng.descriptors(), b)  # deterministic
+        # energy identity E_i = sum_l beta_l B_l (compute_energy, snap_core.hpp:684-701)
         eng.run()
+        e, _ = eng.energy()
+        assert normerr(b @ np.asarray(pr.beta), e) <= 1e-11, name
         assert normerr(eng.forces(), out["forces"]) <= FTOL
         eng.close()
 
