@@ -1090,20 +1090,6 @@ __device__ __forceinline__ void group_sync(int g) {
   }
 }
 constexpr int kYItemCap = 1024;  // row-pair units at 2J = 8: 838 (1479 items)
-#ifndef SNAP_Y_PAIR_U
-#define SNAP_Y_PAIR_U 1
-#endif
-// Window block lengths 1/1: the smallest code (122 KB vs 218 KB of SASS for
-// U = 2/3), which the cold-L2 step needs (bench: Y 104.2 -> 98.1 us at 2000
-// atoms; warm 92 us either way; 256k atoms 7.94 -> 7.66 ms).
-constexpr int kYPairU = SNAP_Y_PAIR_U;  // window block length of the paired loop
-// whole-tile CTAs (3 warp groups, large problems, warm code): block length 2
-// (262k atoms: 7.66 -> 7.56 ms)
-constexpr int kYPairU3 = 2;
-#ifndef SNAP_Y_SINGLE_U
-#define SNAP_Y_SINGLE_U 1  // window block length of the single-item loop
-#endif
-
 // beta-independent tables of the constant-window kernel, in the constant bank
 // of the per-2J object (launch_t.cu, uploaded once per device): warp-uniform
 // reads, so every access is a broadcast from the constant cache.
@@ -1139,133 +1125,74 @@ struct YWArgs {
 // G row-pair items (G = 1, or a pair of items sharing tuple and target row,
 // hence every C' coefficient) accumulated into the row outputs acc[ma]:
 //     acc[ma] += C'(a1, a2) * sum_g W_g x1_g[a1] x2_g[a2],  a1 = ma + D - a2
-// a2 runs over the x2 row; x1 lives in a register window E aligned with
-// the outputs: E[U-1+ma] = x1[ma + D - a2] (current window) and the U-1 slots
-// below hold the elements entering during a block of U steps, so step u of a
-// block reads E[U-1+ma-u] (compile-time index) and only one re-alignment per
-// block is needed.
-template <int G, int U, int L, int JW, int NP, int GW>
-__device__ __forceinline__ void yw_units(const double* __restrict__ sX,
+// a2 runs over the x2 row; every x1 element comes straight from the
+// interleaved X tile (one 16-byte load per element and step).  A register
+// window aligned with the outputs would load one element per step instead,
+// but re-aligning it costs 2(L-1) register moves per item and step and ~1.5x
+// the registers; measured on B200 the direct loads win (2000 atoms: Y 92 ->
+// 84 us; 262k atoms 7.61 -> 7.06 ms), shared-memory bandwidth has headroom.
+#ifndef SNAP_Y_UNROLL
+#define SNAP_Y_UNROLL 2
+#endif
+constexpr int kYUnroll = SNAP_Y_UNROLL;  // a2 steps unrolled (loads of the next step overlap)
+
+template <int G, int L, int JW, int GW>
+__device__ __forceinline__ void yw_units(const double2* __restrict__ sX,
                                          const double* __restrict__ sW, int lane, int b, int e,
                                          double (&ar)[L], double (&ai)[L]) {
   for (int it = b; it < e; ++it) {
     const uint4 m = (GW == 4) ? cYItems4[it] : cYItems12[it];
     const int J2 = m.y & 0xff;
     const double* c0 = cCW + (m.y >> 8);
-    const double* p1[G];
-    const double* p2[G];
+    const double2* p1[G];
+    const double2* p2[G];
     double wt[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const unsigned xb = g == 0 ? m.x : m.z;
-      p1[g] = sX + (kXPad + (xb & 0xffff)) * 32 + lane;  // x1[base + k] at p1[k*32]
-      p2[g] = sX + (kXPad + (xb >> 16)) * 32 + lane;
+      p1[g] = sX + (kXPad + (int)(xb & 0xffff)) * 32 + lane;  // x1[base + k] at p1[k * 32]
+      p2[g] = sX + (kXPad + (int)(xb >> 16)) * 32 + lane;
       wt[g] = sW[m.w + g];
     }
-    double er[G][L + U - 1], ei[G][L + U - 1];
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-      for (int ma = 0; ma < L; ++ma) {
-        er[g][U - 1 + ma] = p1[g][ma * 32];
-        ei[g][U - 1 + ma] = p1[g][(NP + ma) * 32];
-      }
-    int a2 = 0;
-    for (; a2 + U - 1 <= J2; a2 += U) {
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int k = 1; k < U; ++k) {  // x1[D - a2 - k]
-          er[g][U - 1 - k] = p1[g][(-a2 - k) * 32];
-          ei[g][U - 1 - k] = p1[g][(NP - a2 - k) * 32];
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        double x2r[G], x2i[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          x2r[g] = wt[g] * p2[g][(a2 + u) * 32];
-          x2i[g] = wt[g] * p2[g][(NP + a2 + u) * 32];
-        }
-        const double* c = c0 + (a2 + u) * JW;
-#pragma unroll
-        for (int ma = 0; ma < L; ++ma) {
-          const double cc = c[ma];
-          double pr = er[0][U - 1 + ma - u] * x2r[0];
-          double pi = er[0][U - 1 + ma - u] * x2i[0];
-          pr = fma(-ei[0][U - 1 + ma - u], x2i[0], pr);
-          pi = fma(ei[0][U - 1 + ma - u], x2r[0], pi);
-#pragma unroll
-          for (int g = 1; g < G; ++g) {
-            pr = fma(er[g][U - 1 + ma - u], x2r[g], pr);
-            pi = fma(er[g][U - 1 + ma - u], x2i[g], pi);
-            pr = fma(-ei[g][U - 1 + ma - u], x2i[g], pr);
-            pi = fma(ei[g][U - 1 + ma - u], x2r[g], pi);
-          }
-          ar[ma] = fma(cc, pr, ar[ma]);
-          ai[ma] = fma(cc, pi, ai[ma]);
-        }
-      }
-      // re-align: new window = x1[ma + D - a2 - U] = E[ma - 1], E[-1] loaded
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-#pragma unroll
-        for (int ma = L - 1; ma >= 1; --ma) {
-          er[g][U - 1 + ma] = er[g][ma - 1];
-          ei[g][U - 1 + ma] = ei[g][ma - 1];
-        }
-        er[g][U - 1] = p1[g][(-a2 - U) * 32];
-        ei[g][U - 1] = p1[g][(NP - a2 - U) * 32];
-      }
-    }
-    for (; a2 <= J2; ++a2) {  // remainder, one step at a time
+#pragma unroll kYUnroll
+    for (int a2 = 0; a2 <= J2; ++a2) {
       double x2r[G], x2i[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        x2r[g] = wt[g] * p2[g][a2 * 32];
-        x2i[g] = wt[g] * p2[g][(NP + a2) * 32];
+        const double2 v = p2[g][a2 * 32];
+        x2r[g] = wt[g] * v.x;
+        x2i[g] = wt[g] * v.y;
       }
       const double* c = c0 + a2 * JW;
 #pragma unroll
       for (int ma = 0; ma < L; ++ma) {
         const double cc = c[ma];
-        double pr = er[0][U - 1 + ma] * x2r[0];
-        double pi = er[0][U - 1 + ma] * x2i[0];
-        pr = fma(-ei[0][U - 1 + ma], x2i[0], pr);
-        pi = fma(ei[0][U - 1 + ma], x2r[0], pi);
+        const double2 x1 = p1[0][(ma - a2) * 32];
+        double pr = x1.x * x2r[0];
+        double pi = x1.x * x2i[0];
+        pr = fma(-x1.y, x2i[0], pr);
+        pi = fma(x1.y, x2r[0], pi);
 #pragma unroll
         for (int g = 1; g < G; ++g) {
-          pr = fma(er[g][U - 1 + ma], x2r[g], pr);
-          pi = fma(er[g][U - 1 + ma], x2i[g], pi);
-          pr = fma(-ei[g][U - 1 + ma], x2i[g], pr);
-          pi = fma(ei[g][U - 1 + ma], x2r[g], pi);
+          const double2 y = p1[g][(ma - a2) * 32];
+          pr = fma(y.x, x2r[g], pr);
+          pi = fma(y.x, x2i[g], pi);
+          pr = fma(-y.y, x2i[g], pr);
+          pi = fma(y.y, x2r[g], pi);
         }
         ar[ma] = fma(cc, pr, ar[ma]);
         ai[ma] = fma(cc, pi, ai[ma]);
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-#pragma unroll
-        for (int ma = L - 1; ma > 0; --ma) {
-          er[g][U - 1 + ma] = er[g][U - 2 + ma];
-          ei[g][U - 1 + ma] = ei[g][U - 2 + ma];
-        }
-        er[g][U - 1] = p1[g][(-a2 - 1) * 32];
-        ei[g][U - 1] = p1[g][(NP - a2 - 1) * 32];
       }
     }
   }
 }
 
 template <int T, int J, bool MID, int GR>
-__device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __restrict__ sred,
+__device__ __forceinline__ void yw_row(const double2* __restrict__ sX, double* __restrict__ sred,
                                        const double* __restrict__ sW,
                                        int lane, int g, int w, int mb, int rid, const YWArgs& A,
                                        double* __restrict__ Yt, double& e_acc) {
   // g = group, w = warp within the group; sred = the group's slice
-  constexpr int NF = c_full_off(T + 1);
-  constexpr int NP = NF + 2 * kXPad;  // padded plane length
-  constexpr int NH = c_half_off(T + 1);
   constexpr int L = MID ? J / 2 + 1 : J + 1;
   constexpr int JW = J + 1;
   constexpr int nw = kYWarps / GR;
@@ -1274,8 +1201,8 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
   const int* rb = (nw == 4 ? cYRowW4 : cYRowW12) + rid * (2 * nw + 1) + 2 * w;
-  yw_units<2, (GR == 3 ? kYPairU3 : kYPairU), L, JW, NP, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
-  yw_units<1, SNAP_Y_SINGLE_U, L, JW, NP, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);        // singles
+  yw_units<2, L, JW, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
+  yw_units<1, L, JW, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);  // singles
 #pragma unroll
   for (int m = 0; m < L; ++m) {
     sred[((w * (T + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
@@ -1294,7 +1221,8 @@ __device__ __forceinline__ void yw_row(const double* __restrict__ sX, double* __
       const double wgt = (MID && 2 * ma == J) ? 0.5 : 1.0;
       yr *= wgt;
       yi *= wgt;
-      e_acc += yr * sX[(fb + ma) * 32 + lane] + yi * sX[(NP + fb + ma) * 32 + lane];
+      const double2 x = sX[(fb + ma) * 32 + lane];
+      e_acc += yr * x.x + yi * x.y;
     }
     reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
   }
@@ -1308,8 +1236,8 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   constexpr int NP = NF + 2 * kXPad;
   constexpr int NH = c_half_off(T + 1);
   extern __shared__ double smem[];
-  double* sX = smem;                  // [re|im][pad | full idx | pad][32]
-  double* sred = smem + 2 * NP * 32;  // [warp][T+1][re|im][32]
+  double2* sX = reinterpret_cast<double2*>(smem);  // [pad | full idx | pad][32] (re, im)
+  double* sred = smem + 2 * NP * 32;               // [warp][T+1][re|im][32]
   double* sW = sred + kYWarps * (T + 1) * 2 * 32;  // W per item
   __shared__ double se[kYWarps][32];
 #ifdef SNAP_Y_PROFILE
@@ -1321,8 +1249,8 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   const int tile = blockIdx.x;
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
   for (int e = threadIdx.x; e < kXPad * 32; e += blockDim.x) {
-    sX[e] = sX[(kXPad + NF) * 32 + e] = 0.0;
-    sX[NP * 32 + e] = sX[(NP + kXPad + NF) * 32 + e] = 0.0;
+    sX[e] = make_double2(0.0, 0.0);
+    sX[(kXPad + NF) * 32 + e] = make_double2(0.0, 0.0);
   }
   {
     // Half stack -> full mirrored X: warp w takes half elements h = w + nw k
@@ -1347,13 +1275,11 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     for (int k = 0; k < KH; ++k) {
       const int h = wq + kYWarps * k;
       if (h < NH) {
-        sX[(kXPad + sc[k].x) * 32 + ln] = re[k];
-        sX[(NP + kXPad + sc[k].x) * 32 + ln] = im[k];
+        sX[(kXPad + sc[k].x) * 32 + ln] = make_double2(re[k], im[k]);
         if (sc[k].y >= 0) {
           const int fm = sc[k].y >> 1;
           const bool neg = sc[k].y & 1;
-          sX[(kXPad + fm) * 32 + ln] = neg ? -re[k] : re[k];
-          sX[(NP + kXPad + fm) * 32 + ln] = neg ? im[k] : -im[k];
+          sX[(kXPad + fm) * 32 + ln] = neg ? make_double2(-re[k], im[k]) : make_double2(re[k], -im[k]);
         }
       }
     }

@@ -3,6 +3,8 @@ import sys, time
 import numpy as np
 sys.path.insert(0, '.')
 import paper_2011_12875_b200 as snap
+if len(sys.argv) > 1 and sys.argv[1].startswith("--lib="):  # A/B builds (make OUT=... EXTRA=...)
+    snap.LIB_PATH = sys.argv.pop(1)[6:]
 
 def run(nx, ny, nz, T=8, reps=10, tune=None):
     p = snap.bcc_problem(nx, ny, nz, twojmax=T)
