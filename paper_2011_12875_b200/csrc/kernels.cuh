@@ -1140,8 +1140,10 @@ template <int G, int L, int JW, int GW>
 __device__ __forceinline__ void yw_units(const double2* __restrict__ sX,
                                          const double* __restrict__ sW, int lane, int b, int e,
                                          double (&ar)[L], double (&ai)[L]) {
+  uint4 nxt = b < e ? ((GW == 4) ? cYItems4[b] : cYItems12[b]) : make_uint4(0u, 0u, 0u, 0u);
   for (int it = b; it < e; ++it) {
-    const uint4 m = (GW == 4) ? cYItems4[it] : cYItems12[it];
+    const uint4 m = nxt;  // the next record is in flight during this unit
+    if (it + 1 < e) nxt = (GW == 4) ? cYItems4[it + 1] : cYItems12[it + 1];
     const int J2 = m.y & 0xff;
     const double* c0 = cCW + (m.y >> 8);
     const double2* p1[G];
@@ -1303,7 +1305,7 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     const int code = __ldg(tasks + q);
     if (code < 0) break;
     const int j = code >> 6, mb = code & 63;
-    const int rid = c_acc_off(j) + mb;
+    const int rid = (j * j + 2 * j + (j & 1)) / 4 + mb;  // c_acc_off(j) + mb
 #define YWROW(JJ)                                                                       \
   case JJ:                                                                              \
     if constexpr (JJ <= T) {                                                            \
