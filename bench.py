@@ -419,7 +419,25 @@ def run_ours(args):
             t_e2e = float(tt.item())
         e2e = {"value": N * args.steps / t_e2e / 1000.0, "unit": "Katom-steps/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": t_e2e * 1e3 / args.steps}
+               "ms_per_step": t_e2e * 1e3 / args.steps,
+               "path": "snapgpu_run_host: neighbor lists in, forces/energies out"}
+        if n_gpus == 1:
+            # the MD-loop call: positions in (neighbor lists rebuilt on the
+            # device every step inside the same graph), forces/energies out
+            pos_h = torch.from_numpy(np.ascontiguousarray(p.positions)).pin_memory().numpy()
+            for _ in range(max(1, args.warmup // 2)):
+                eng.step_positions(pos_h, p.box, forces=f_host, eatom=e_host, etotal=t_host)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                eng.step_positions(pos_h, p.box, forces=f_host, eatom=e_host, etotal=t_host)
+            t_pos = time.perf_counter() - t0
+            e2e["positions"] = {"value": N * args.steps / t_pos / 1000.0,
+                                "unit": "Katom-steps/s", "h2d_bytes_per_step": int(pos_h.nbytes),
+                                "d2h_bytes_per_step": int(d2h),
+                                "ms_per_step": t_pos * 1e3 / args.steps,
+                                "path": "snapgpu_run_positions: positions in, lists rebuilt "
+                                        "on the device in the step graph, forces/energies out"}
 
     # ---- FP64 issue-rate probe on this box --------------------------------
     probe = None

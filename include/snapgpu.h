@@ -146,6 +146,21 @@ int snapgpu_set_positions(snapgpu_ctx* ctx, int natoms, const double* pos,
                           const double* box);
 int snapgpu_get_neighbors(snapgpu_ctx* ctx, int* numneigh, int* nbr, double* disp);
 
+/* One force step from host POSITIONS (the MD-loop call): the positions
+ * (natoms x 3, any image, orthorhombic box[3]) are staged into pinned
+ * memory, then ONE CUDA graph uploads them, rebuilds the neighbor lists on
+ * the device (as snapgpu_set_positions, with the current stride as capacity:
+ * no host round trip), derives the partner slots of the symmetric lists,
+ * runs U -> Y(+E) -> fused dU/dE -> deterministic force gather and reads
+ * forces (natoms x 3), eatom and etotal back; one stream synchronization.
+ * The first call (or a new atom count / box, or a list outgrowing the
+ * stride) takes the snapgpu_set_positions path first.  Any output may be
+ * NULL.  Equivalent to build_neighborlist (harness.hpp:119-202) followed by
+ * run_pipeline (pipeline.hpp:206-303). */
+int snapgpu_run_positions(snapgpu_ctx* ctx, int natoms, const double* pos,
+                          const double* box, double* forces, double* eatom,
+                          double* etotal);
+
 /* Bispectrum descriptors B_l(i) (compute_B_from_U,
  * snap_core.hpp:642-681, b_contract :556-575) of the owned atoms,
  * blist[i * ntriples + l], in one pass over Ulisttot (k_compute_B: every

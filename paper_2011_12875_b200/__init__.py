@@ -91,6 +91,7 @@ def library() -> C.CDLL:
     L.snapgpu_get_virial.argtypes = [vp, vp]
     L.snapgpu_compute_descriptors.argtypes = [vp, vp]
     L.snapgpu_set_positions.argtypes = [vp, ip, vp, vp]
+    L.snapgpu_run_positions.argtypes = [vp, ip, vp, vp, vp, vp, vp]
     L.snapgpu_get_neighbors.argtypes = [vp, vp, vp, vp]
     L.snapgpu_device_outputs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
     L.snapgpu_get_forces_device.argtypes = [vp, vp]
@@ -427,6 +428,22 @@ class SnapEngine:
         self.nlocal = self.natoms_total = int(pos.shape[0])
         self.stride = int(self.neighbors(counts_only=True).max(initial=0))
         return self
+
+    def step_positions(self, positions, box, forces=None, eatom=None, etotal=None):
+        """One end-to-end force step from host positions (snapgpu_run_positions):
+        one graph uploads them, rebuilds the neighbor lists on the device,
+        runs the force step and reads the results back.  Returns
+        (forces, eatom, etotal)."""
+        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+        n = int(pos.shape[0])
+        bx = np.ascontiguousarray(np.broadcast_to(np.asarray(box, np.float64), (3,)))
+        f = forces if forces is not None else np.zeros((n, 3), np.float64)
+        e = eatom if eatom is not None else np.zeros(n, np.float64)
+        t = etotal if etotal is not None else np.zeros(1, np.float64)
+        self._c(self._L.snapgpu_run_positions(self._h, n, pos.ctypes.data, bx.ctypes.data,
+                                              f.ctypes.data, e.ctypes.data, t.ctypes.data))
+        self.natoms_total = self.nlocal = n
+        return f, e, float(t[0])
 
     def neighbors(self, counts_only=False):
         """(numneigh, nbr, disp) of the current lists, read back from the device."""

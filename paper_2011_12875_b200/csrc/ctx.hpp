@@ -132,6 +132,7 @@ struct snapgpu_ctx {
   // neighbor index, rebuilt when the lists change
   snapgpu::host::DevBuf<int> d_rev_off, d_rev_cur, d_rev;
   bool csr_dirty = true;
+  bool sym_lists = false;  // lists built on the device: symmetric, partner slots in d_rev
   // force output layout: nchunks chunks of chunk_rows atoms (+ energy slot
   // when nchunks > 1), into the caller's device buffer when ext_forces is set
   int nchunks = 1;
@@ -147,6 +148,12 @@ struct snapgpu_ctx {
   bool graph_valid = false;
   cudaGraph_t csr_graph = nullptr;
   cudaGraphExec_t csr_gexec = nullptr;
+  // one-call positions step (snapgpu_run_positions): pinned staging + graph
+  cudaGraph_t pos_graph = nullptr;
+  cudaGraphExec_t pos_gexec = nullptr;
+  double* h_pos = nullptr;
+  size_t h_pos_n = 0;
+  double nl_box[3] = {0, 0, 0};
 
   // timing
   bool timing = false;

@@ -1675,8 +1675,10 @@ __global__ void __launch_bounds__(256) k_rev_sort(const RevArgs A) {
 // both the partial forces and the energies (distributed.py).
 struct GatherArgs {
   PairArgs pr;
-  const int* off;
-  const int* rev;
+  const int* off;     // CSR offsets (rev_stride == 0)
+  const int* rev;     // reverse slots: CSR, or per own slot its partner slot
+  int rev_stride;     // > 0: symmetric lists, atom a's reverse slots are
+                      // rev[a*stride + k], k < numneigh[a] (k_nl_partner)
   const double* dedr;
   double* forces;
   int chunk_rows, chunk_stride, nchunks;
@@ -1704,8 +1706,16 @@ __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
     return;
   }
   const int S = A.pr.stride;
-  const int s0 = A.off[a], nrev = A.off[a + 1] - s0;
   const int il = a - A.pr.atom_lo;
+  int s0, nrev;
+  if (A.rev_stride > 0) {  // symmetric lists: the partners of the own row, in its order
+    s0 = a * A.rev_stride;
+    nrev = A.pr.numneigh[a];
+    nrev = (nrev < 0 || nrev > S) ? 0 : nrev;
+  } else {
+    s0 = A.off[a];
+    nrev = A.off[a + 1] - s0;
+  }
   int nn = 0, own = 0;
   if (il >= 0 && il < A.pr.nlocal) {
     own = il * S;
@@ -1831,6 +1841,9 @@ __device__ __forceinline__ double nl_wrap(double x, double box) {
   return w >= box ? __dsub_rn(w, box) : w;
 }
 __device__ __forceinline__ double nl_min_image(double d, double box) {
+  // |d| <= box/2 (exact test) => rint(d/box) = 0 and the formula returns d
+  // unchanged: skip the division (bitwise the same result)
+  if (fabs(d) * 2.0 <= box) return d;
   return __dsub_rn(d, __dmul_rn(box, rint(__ddiv_rn(d, box))));
 }
 
@@ -1852,33 +1865,44 @@ __global__ void k_nl_bin(const NLArgs A) {
   }
 }
 
-// exclusive offsets: head[c] = sum of counts of cells < c (one CTA)
+// exclusive offsets: head[c] = sum of counts of cells < c, head[ncell] = total
+// (one CTA of 1024 threads: per-thread chunk sums, a warp-shuffle block scan,
+// then each thread rewrites its chunk); counts arrive in head[c+1]; fill[c]
+// receives the same offsets (cursors).
 __global__ void __launch_bounds__(1024) k_nl_scan(int* head, int ncell, int* fill) {
-  __shared__ int part[1024];
-  const int t = threadIdx.x, nt = blockDim.x;
+  __shared__ int wsum[32];
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5;
   const int per = (ncell + nt - 1) / nt;
   const int b = min(ncell, t * per), e = min(ncell, b + per);
   int s = 0;
   for (int c = b; c < e; ++c) s += head[c + 1];
-  part[t] = s;
+  int x = s;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += v;
+  }
+  if (lane == 31) wsum[w] = x;
   __syncthreads();
-  if (t == 0) {
-    int acc = 0;
-    for (int q = 0; q < nt; ++q) {
-      const int v = part[q];
-      part[q] = acc;
-      acc += v;
+  if (w == 0) {
+    int y = lane < (nt >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += v;
     }
+    wsum[lane] = y;  // inclusive over warps
   }
   __syncthreads();
-  int acc = part[t];
+  int acc = x - s + (w > 0 ? wsum[w - 1] : 0);  // exclusive prefix of this chunk
+  __syncthreads();  // every thread has read its counts before any rewrite
   for (int c = b; c < e; ++c) {
     const int v = head[c + 1];
     head[c] = acc;  // head[c] read only by this thread (c in [b, e))
     fill[c] = acc;
     acc += v;
   }
-  if (e == ncell && b < e) head[ncell] = acc;
+  if (t == nt - 1) head[ncell] = (w > 0 ? wsum[(nt >> 5) - 1] : x);
   if (ncell == 0 && t == 0) head[0] = 0;
 }
 
@@ -1888,67 +1912,112 @@ __global__ void k_nl_members(const NLArgs A) {
   A.members[atomicAdd(A.fill + A.cell_of[i], 1)] = i;
 }
 
-// PASS 1: count (and max); PASS 2: collect, sort by index, write.
-template <int PASS>
-__global__ void __launch_bounds__(128) k_nl_lists(const NLArgs A) {
-  constexpr int kCap = 128;  // per-atom candidates held for the sort
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// Warp-per-atom list build (set_positions pass 2 and the sync-free one-call
+// positions step): lane c < 27 scans cell c of the atom's stencil, the hits
+// are compacted into a shared buffer, ranked (neighbor indices are distinct)
+// and written sorted with the same arithmetic as k_nl_lists.  numneigh is the
+// true count; a count above the stride (the capacity) raises kErrCount and
+// writes no list (the host then re-plans with a larger stride).
+constexpr int kNLWarps = 4;
+__global__ void __launch_bounds__(kNLWarps * 32) k_nl_lists_warp(const NLArgs A, unsigned* err) {
+  constexpr int kCap = 128;
+  __shared__ int sbuf[kNLWarps][kCap];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int i = blockIdx.x * kNLWarps + wl;
   if (i >= A.n) return;
+  int* buf = sbuf[wl];
   const double xi = A.w[i * 3], yi = A.w[i * 3 + 1], zi = A.w[i * 3 + 2];
-  int cnt = 0;
-  int idx[PASS == 2 ? kCap : 1];
-  auto consider = [&](int k) {
+  auto inside = [&](int k) {
     const double dx = nl_min_image(__dsub_rn(A.w[k * 3], xi), A.box[0]);
     const double dy = nl_min_image(__dsub_rn(A.w[k * 3 + 1], yi), A.box[1]);
     const double dz = nl_min_image(__dsub_rn(A.w[k * 3 + 2], zi), A.box[2]);
     const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-    if (r2 < A.rc2) {
-      if (PASS == 2 && cnt < kCap) idx[cnt] = k;
-      ++cnt;
-    }
+    return r2 < A.rc2;
   };
-  if (A.cells) {
+  // candidates: lane c scans stencil cell c (or, without cells, atoms lane +
+  // 32 q); two passes over the same candidates: count, then write at the
+  // lane's offset (no per-lane buffers)
+  int s0 = 0, s1 = 0;
+  if (A.cells && lane < 27) {
     const int c = A.cell_of[i];
     const int cx = c % A.nc[0], cy = (c / A.nc[0]) % A.nc[1], cz = c / (A.nc[0] * A.nc[1]);
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int ox = (cx + dx + A.nc[0]) % A.nc[0], oy = (cy + dy + A.nc[1]) % A.nc[1],
-                    oz = (cz + dz + A.nc[2]) % A.nc[2];
-          const int oc = (oz * A.nc[1] + oy) * A.nc[0] + ox;
-          for (int s = A.head[oc]; s < A.head[oc + 1]; ++s) {
-            const int k = A.members[s];
-            if (k != i) consider(k);
-          }
-        }
-  } else {
-    for (int k = 0; k < A.n; ++k)
-      if (k != i) consider(k);
+    const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
+    const int ox = (cx + dx + A.nc[0]) % A.nc[0], oy = (cy + dy + A.nc[1]) % A.nc[1],
+              oz = (cz + dz + A.nc[2]) % A.nc[2];
+    const int oc = (oz * A.nc[1] + oy) * A.nc[0] + ox;
+    s0 = A.head[oc];
+    s1 = A.head[oc + 1];
   }
-  if (PASS == 1) {
-    A.numneigh[i] = cnt;
-    atomicMax(A.maxcount, cnt);
+  auto scan = [&](auto&& f) {
+    if (A.cells) {
+      for (int s = s0; s < s1; ++s) {
+        const int k = A.members[s];
+        if (k != i && inside(k)) f(k);
+      }
+    } else {
+      for (int k = lane; k < A.n; k += 32)
+        if (k != i && inside(k)) f(k);
+    }
+  };
+  int mine = 0;
+  scan([&](int) { ++mine; });
+  int cnt = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {  // inclusive scan of the counts
+    const int v = __shfl_up_sync(0xffffffffu, cnt, o);
+    if (lane >= o) cnt += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, cnt, 31);
+  int off = cnt - mine;
+  if (lane == 0) {
+    A.numneigh[i] = total;
+    if (A.maxcount) atomicMax(A.maxcount, total);
+  }
+  if (!A.nbr) return;  // count pass
+  if (total > A.stride || total > kCap) {
+    if (lane == 0) atomicOr(err, kErrCount);
     return;
   }
-  // insertion sort by neighbor index (harness.hpp: lists sorted by index)
-  const int m = min(cnt, kCap);
-  for (int a = 1; a < m; ++a) {
-    const int v = idx[a];
-    int b = a - 1;
-    while (b >= 0 && idx[b] > v) {
-      idx[b + 1] = idx[b];
-      --b;
-    }
-    idx[b + 1] = v;
+  scan([&](int k) { buf[off++] = k; });
+  __syncwarp();
+  // rank sort of the distinct indices, then write in index order
+  for (int q = lane; q < total; q += 32) {
+    const int v = buf[q];
+    int rank = 0;
+    for (int r = 0; r < total; ++r) rank += (buf[r] < v) ? 1 : 0;
+    const size_t pk = (size_t)i * A.stride + rank;
+    A.nbr[pk] = v;
+    A.disp[pk * 3 + 0] = nl_min_image(__dsub_rn(A.w[v * 3], xi), A.box[0]);
+    A.disp[pk * 3 + 1] = nl_min_image(__dsub_rn(A.w[v * 3 + 1], yi), A.box[1]);
+    A.disp[pk * 3 + 2] = nl_min_image(__dsub_rn(A.w[v * 3 + 2], zi), A.box[2]);
   }
-  for (int q = 0; q < m; ++q) {
-    const int k = idx[q];
-    const size_t pk = (size_t)i * A.stride + q;
-    A.nbr[pk] = k;
-    A.disp[pk * 3 + 0] = nl_min_image(__dsub_rn(A.w[k * 3], xi), A.box[0]);
-    A.disp[pk * 3 + 1] = nl_min_image(__dsub_rn(A.w[k * 3 + 1], yi), A.box[1]);
-    A.disp[pk * 3 + 2] = nl_min_image(__dsub_rn(A.w[k * 3 + 2], zi), A.box[2]);
+}
+
+// Partner slots of symmetric, index-sorted lists (the device-built ones:
+// min_image is odd and r2 symmetric, so j is in i's list iff i is in j's):
+// for own slot (i, k) with j = nbr(i, k), rev[i*S + k] = j*S + (position of
+// i in j's list), found by binary search.  This is the reverse-neighbor
+// index for k_gather_forces (rev_stride = S) without the CSR build.
+__global__ void __launch_bounds__(256) k_nl_partner(const int* numneigh, const int* nbr, int n,
+                                                    int S, int* rev, unsigned* err) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n * S) return;
+  const int i = p / S, k = p - i * S;
+  const int nn = numneigh[i];
+  if (nn > S || k >= nn) return;
+  const int j = nbr[p];
+  const int* row = nbr + (size_t)j * S;
+  int lo = 0, hi = min(numneigh[j], S) - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (row[mid] < i) lo = mid + 1;
+    else hi = mid;
   }
+  if (hi < 0 || row[lo] != i) {  // not symmetric: cannot happen for built lists
+    atomicOr(err, kErrIndex);
+    return;
+  }
+  rev[p] = j * S + lo;
 }
 
 // FP64 issue-rate probe: 8 independent DFMA chains per thread.

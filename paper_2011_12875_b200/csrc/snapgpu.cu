@@ -21,6 +21,13 @@ void invalidate_graph(snapgpu_ctx* c) {
   c->graph_valid = false;
 }
 
+void invalidate_pos_graph(snapgpu_ctx* c) {
+  if (c->pos_gexec) cudaGraphExecDestroy(c->pos_gexec);
+  if (c->pos_graph) cudaGraphDestroy(c->pos_graph);
+  c->pos_gexec = nullptr;
+  c->pos_graph = nullptr;
+}
+
 template <class F>
 int guarded(snapgpu_ctx* c, F&& f) {
   try {
@@ -209,7 +216,7 @@ void invalidate_csr_graph(snapgpu_ctx* c) {
 // Rebuild the reverse index if the lists changed since the last build (a
 // captured graph of its five stream operations, replayed per list upload).
 void ensure_csr(snapgpu_ctx* c) {
-  if (!c->csr_dirty) return;
+  if (!c->csr_dirty || c->sym_lists) return;
   if (!c->csr_gexec) {
     cudaStream_t user = c->stream;
     c->stream = c->own_stream;
@@ -237,6 +244,7 @@ void launch_gather(snapgpu_ctx* c) {
   a.pr = pair_args(c);
   a.off = c->d_rev_off.p;
   a.rev = c->d_rev.p;
+  a.rev_stride = c->sym_lists ? c->stride : 0;
   a.dedr = c->d_dedr.p;
   a.forces = forces_ptr(c);
   a.chunk_rows = c->chunk_rows();
@@ -277,12 +285,14 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
           "problem: null neighbor arrays");
   c->have_lists = c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
   c->csr_dirty = true;
+  c->sym_lists = false;
   const bool reshape = natoms_total != c->natoms_total || nlocal != c->nlocal ||
                        stride != c->stride || atom_lo != c->atom_lo ||
                        (types != nullptr) != (c->d_types.p != nullptr);
   if (reshape) {
     invalidate_graph(c);
     invalidate_csr_graph(c);
+    invalidate_pos_graph(c);
   }
   c->natoms_total = natoms_total;
   c->atom_lo = atom_lo;
@@ -373,6 +383,66 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
     require(cut_ok, "problem: neighbor at or beyond Rcut");
   }
   c->have_lists = true;
+}
+
+// Device neighbor lists (kernels.cuh k_nl_*): argument block, scratch
+// allocations and the front half (positions upload, cell binning, cell
+// offsets, members) shared by set_positions and the one-call positions step.
+NLArgs nl_setup(snapgpu_ctx* c, int natoms, const double* pos, const double* box) {
+  require(natoms >= 0 && (natoms == 0 || pos) && box, "set_positions: bad arguments");
+  const double rcut = c->gp.rcut;
+  NLArgs a{};
+  for (int d = 0; d < 3; ++d) {  // harness.hpp:119-125 preconditions
+    require(box[d] > 0.0 && rcut > 0.0, "build_neighborlist: box and Rcut must be positive");
+    require(rcut <= 0.5 * box[d], "build_neighborlist: Rcut must not exceed box/2");
+    a.box[d] = box[d];
+    a.nc[d] = static_cast<int>(std::floor(box[d] / rcut));
+  }
+  a.cells = (a.nc[0] >= 3 && a.nc[1] >= 3 && a.nc[2] >= 3) ? 1 : 0;
+  a.n = natoms;
+  a.rc2 = rcut * rcut;
+  const long ncell = a.cells ? (long)a.nc[0] * a.nc[1] * a.nc[2] : 0;
+  c->d_nlpos.alloc(std::max<size_t>(1, (size_t)natoms * 6));
+  c->d_nlint.alloc((size_t)std::max(1, natoms) * 3 + 2 * (size_t)ncell + 4);
+  double* dpos = c->d_nlpos.p;
+  a.pos = dpos;
+  a.w = dpos + (size_t)natoms * 3;
+  int* ib = c->d_nlint.p;
+  a.cell_of = ib;
+  a.members = ib + natoms;
+  a.numneigh = ib + 2 * (size_t)natoms;
+  a.head = ib + 3 * (size_t)natoms;
+  a.fill = a.head + ncell + 1;
+  a.maxcount = a.fill + ncell;
+  return a;
+}
+
+void nl_front(snapgpu_ctx* c, const NLArgs& a, const double* host_pos) {
+  const long ncell = a.cells ? (long)a.nc[0] * a.nc[1] * a.nc[2] : 0;
+  if (a.n > 0)
+    CK(cudaMemcpyAsync(const_cast<double*>(a.pos), host_pos, sizeof(double) * 3 * a.n,
+                       cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(a.head, 0, sizeof(int) * (ncell + 1), c->stream));
+  const int blk = (a.n + 127) / 128;
+  if (a.n > 0) {
+    k_nl_bin<<<blk, 128, 0, c->stream>>>(a);
+    if (a.cells) {
+      k_nl_scan<<<1, 1024, 0, c->stream>>>(a.head, (int)ncell, a.fill);
+      k_nl_members<<<blk, 128, 0, c->stream>>>(a);
+    }
+    CK(cudaGetLastError());
+  }
+}
+
+// partner slots of the (symmetric) device-built lists into d_rev
+void launch_partner(snapgpu_ctx* c) {
+  const int ns = c->nlocal * c->stride;
+  if (ns > 0) {
+    k_nl_partner<<<(ns + 255) / 256, 256, 0, c->stream>>>(c->d_numneigh.p, c->d_nbr.p,
+                                                          c->nlocal, c->stride, c->d_rev.p,
+                                                          c->d_err.p);
+    CK(cudaGetLastError());
+  }
 }
 
 void record(snapgpu_ctx* c, int k) {
@@ -507,6 +577,8 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   invalidate_csr_graph(c);
+  invalidate_pos_graph(c);
+  if (c->h_pos) cudaFreeHost(c->h_pos);
   c->d_weights.release();
   c->d_cw.release();
 
@@ -837,42 +909,12 @@ int snapgpu_get_ylist(snapgpu_ctx* c, double* out) {
 int snapgpu_set_positions(snapgpu_ctx* c, int natoms, const double* pos, const double* box) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
-    require(natoms >= 0 && (natoms == 0 || pos) && box, "set_positions: bad arguments");
-    const double rcut = c->gp.rcut;
-    NLArgs a{};
-    for (int d = 0; d < 3; ++d) {  // harness.hpp:119-125 preconditions
-      require(box[d] > 0.0 && rcut > 0.0, "build_neighborlist: box and Rcut must be positive");
-      require(rcut <= 0.5 * box[d], "build_neighborlist: Rcut must not exceed box/2");
-      a.box[d] = box[d];
-      a.nc[d] = static_cast<int>(std::floor(box[d] / rcut));
-    }
-    a.cells = (a.nc[0] >= 3 && a.nc[1] >= 3 && a.nc[2] >= 3) ? 1 : 0;
-    a.n = natoms;
-    a.rc2 = rcut * rcut;
-    const long ncell = a.cells ? (long)a.nc[0] * a.nc[1] * a.nc[2] : 0;
-    c->d_nlpos.alloc(std::max<size_t>(1, (size_t)natoms * 6));
-    c->d_nlint.alloc((size_t)std::max(1, natoms) * 3 + 2 * (size_t)ncell + 4);
-    double* dpos = c->d_nlpos.p;
-    a.pos = dpos;
-    a.w = dpos + (size_t)natoms * 3;
-    int* ib = c->d_nlint.p;
-    a.cell_of = ib;
-    a.members = ib + natoms;
-    a.numneigh = ib + 2 * (size_t)natoms;
-    a.head = ib + 3 * (size_t)natoms;
-    a.fill = a.head + ncell + 1;
-    a.maxcount = a.fill + ncell;
-    CK(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * natoms, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemsetAsync(a.head, 0, sizeof(int) * (ncell + 1), c->stream));
+    NLArgs a = nl_setup(c, natoms, pos, box);
+    nl_front(c, a, pos);
     CK(cudaMemsetAsync(a.maxcount, 0, sizeof(int), c->stream));
-    const int blk = (natoms + 127) / 128;
-    if (natoms > 0) {
-      k_nl_bin<<<blk, 128, 0, c->stream>>>(a);
-      if (a.cells) {
-        k_nl_scan<<<1, 1024, 0, c->stream>>>(a.head, (int)ncell, a.fill);
-        k_nl_members<<<blk, 128, 0, c->stream>>>(a);
-      }
-      k_nl_lists<1><<<blk, 128, 0, c->stream>>>(a);
+    const int wblk = (natoms + kNLWarps - 1) / kNLWarps;
+    if (natoms > 0) {  // count pass (a.nbr == nullptr)
+      k_nl_lists_warp<<<wblk, kNLWarps * 32, 0, c->stream>>>(a, c->d_err.p);
       CK(cudaGetLastError());
     }
     int mx = 0;
@@ -890,11 +932,111 @@ int snapgpu_set_positions(snapgpu_ctx* c, int natoms, const double* pos, const d
       if (mx > 0) {
         CK(cudaMemsetAsync(c->d_nbr.p, 0, sizeof(int) * (size_t)natoms * mx, c->stream));
         CK(cudaMemsetAsync(c->d_disp.p, 0, sizeof(double) * (size_t)natoms * mx * 3, c->stream));
-        k_nl_lists<2><<<blk, 128, 0, c->stream>>>(a);
+        a.maxcount = nullptr;
+        k_nl_lists_warp<<<wblk, kNLWarps * 32, 0, c->stream>>>(a, c->d_err.p);
         CK(cudaGetLastError());
+        launch_partner(c);
       }
     }
+    // device-built lists are symmetric and sorted: the force gather takes the
+    // partner slots instead of a reverse-neighbor CSR
+    c->sym_lists = true;
+    c->csr_dirty = false;
+    for (int d = 0; d < 3; ++d) c->nl_box[d] = box[d];
   });
+}
+
+int snapgpu_run_positions(snapgpu_ctx* c, int natoms, const double* pos, const double* box,
+                          double* forces, double* eatom, double* etotal) {
+  if (!c) return SNAPGPU_EINVAL;
+  bool fast = c->have_lists && c->sym_lists && natoms == c->natoms_total &&
+              natoms == c->nlocal && c->atom_lo == 0 && c->nchunks == 1 && !c->timing &&
+              box != nullptr && pos != nullptr;
+  if (fast)
+    for (int d = 0; d < 3; ++d) fast = fast && box[d] == c->nl_box[d];
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (!fast) {  // (re)establish stride, cells and shapes: lists with a host sync
+      const int rc = snapgpu_set_positions(c, natoms, pos, box);
+      if (rc != SNAPGPU_OK) return rc;
+    }
+    bool overflow = false;
+    const int rc = guarded(c, [&] {
+      require(natoms > 0, "run_positions: no atoms");
+      const size_t nf = c->d_forces.n, ne = c->d_eatom.n, nout = nf + ne + 1;
+      if (c->h_out_n < nout) {
+        if (c->h_out) cudaFreeHost(c->h_out);
+        c->h_out = nullptr;
+        c->h_out_n = 0;
+        CK(cudaMallocHost(&c->h_out, nout * sizeof(double)));
+        c->h_out_n = nout;
+        invalidate_pos_graph(c);
+      }
+      if (c->h_pos_n < (size_t)natoms * 3) {
+        if (c->h_pos) cudaFreeHost(c->h_pos);
+        c->h_pos = nullptr;
+        c->h_pos_n = 0;
+        CK(cudaMallocHost(&c->h_pos, sizeof(double) * 3 * natoms));
+        c->h_pos_n = (size_t)natoms * 3;
+        invalidate_pos_graph(c);
+      }
+      std::memcpy(c->h_pos, pos, sizeof(double) * 3 * natoms);
+      if (!c->pos_gexec) {  // one graph: H2D, lists, partners, U, Y, dE, gather, D2H
+        cudaStream_t user = c->stream;
+        c->stream = c->own_stream;
+        CK(cudaStreamSynchronize(user));
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          NLArgs a = nl_setup(c, natoms, c->h_pos, c->nl_box);
+          nl_front(c, a, c->h_pos);
+          a.numneigh = c->d_numneigh.p;
+          a.nbr = c->d_nbr.p;
+          a.disp = c->d_disp.p;
+          a.stride = c->stride;
+          a.maxcount = nullptr;
+          k_nl_lists_warp<<<(natoms + kNLWarps - 1) / kNLWarps, kNLWarps * 32, 0, c->stream>>>(
+              a, c->d_err.p);
+          CK(cudaGetLastError());
+          launch_partner(c);
+          run_direct(c);
+          CK(cudaMemcpyAsync(c->h_out, c->d_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+          CK(cudaMemcpyAsync(c->h_err, c->d_err.p, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                             c->stream));
+        } catch (...) {
+          cudaGraph_t g;
+          cudaStreamEndCapture(c->stream, &g);
+          if (g) cudaGraphDestroy(g);
+          c->stream = user;
+          throw;
+        }
+        CK(cudaStreamEndCapture(c->stream, &c->pos_graph));
+        CK(cudaGraphInstantiate(&c->pos_gexec, c->pos_graph, 0));
+        c->stream = user;
+      }
+      CK(cudaGraphLaunch(c->pos_gexec, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      c->have_U = c->have_Y = c->have_dE = c->have_forces = true;
+      if (*c->h_err) {
+        const unsigned f = *c->h_err;
+        CK(cudaMemsetAsync(c->d_err.p, 0, sizeof(unsigned), c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
+        if ((f & kErrCount) && attempt == 0) {  // a list outgrew the stride: rebuild
+          overflow = true;
+          return;
+        }
+        c->have_lists = false;
+        throw InvalidArg{device_error_message(f)};
+      }
+      if (forces) std::memcpy(forces, c->h_out, sizeof(double) * force_doubles(c));
+      if (eatom) std::memcpy(eatom, c->h_out + nf, sizeof(double) * c->nlocal);
+      if (etotal) *etotal = c->h_out[nf + ne];
+    });
+    if (rc != SNAPGPU_OK) return rc;
+    if (!overflow) return SNAPGPU_OK;
+    fast = false;
+  }
+  return SNAPGPU_OK;
 }
 
 int snapgpu_get_neighbors(snapgpu_ctx* c, int* numneigh, int* nbr, double* disp) {
@@ -1040,6 +1182,7 @@ int snapgpu_tune(snapgpu_ctx* c, int y_parts) {
     require(y_parts >= 0 && y_parts <= kMaxYParts, "tune: y_parts must be in [0, 8]");
     c->y_parts = y_parts;
     invalidate_graph(c);
+    invalidate_pos_graph(c);
     if (c->have_lists) plan_y(c);
   });
 }

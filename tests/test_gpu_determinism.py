@@ -118,3 +118,37 @@ def test_forces_match_finite_differences(snap, port, T):
                 fd[i, d] = -(e[0] - e[1]) / (2.0 * h)
     denom = np.maximum(np.maximum(np.abs(f), np.abs(fd)), 1e-14)
     assert float(np.max(np.abs(f - fd) / denom)) <= 1e-5
+
+
+def test_one_call_positions_step(snap):
+    """snapgpu_run_positions (lists rebuilt on the device inside one graph,
+    partner slots instead of the CSR) equals the host-list step bitwise on
+    the same lists, stays exact when the atoms move, and re-plans when a
+    list outgrows the stride."""
+    p = snap.bcc_problem(10, 10, 10, twojmax=8)
+    ref = snap.run_pipeline(p)
+    with snap.SnapEngine.for_problem(p) as eng:
+        for _ in range(3):  # slow path, then graph replays
+            f, e, t = eng.step_positions(p.positions, p.box)
+            assert np.array_equal(f, ref.forces) and np.array_equal(e, ref.eatom)
+            assert t == ref.etotal
+        rng = np.random.default_rng(3)
+        for it in range(3):  # moving atoms: lists rebuilt every step
+            q = p.positions + rng.uniform(-0.02, 0.02, p.positions.shape)
+            f, e, t = eng.step_positions(q, p.box)
+            nn, nbr, disp = snap.build_neighborlist(q, p.box, p.rcut)
+            pr = snap.Problem.from_any(p)
+            pr.numneigh, pr.nbr, pr.disp = nn, nbr, disp
+            r = snap.run_pipeline(pr)
+            assert np.array_equal(f, r.forces) and t == r.etotal
+        # a list outgrowing the stride inside the graph: expand the lattice
+        # (14 neighbors, stride 14), then the original spacing in that box
+        box2 = p.box * 1.05
+        eng.step_positions(p.positions * 1.05, box2)
+        f, e, t = eng.step_positions(p.positions, box2)
+        nn, nbr, disp = snap.build_neighborlist(p.positions, box2, p.rcut)
+        assert nn.max() > 14
+        pr = snap.Problem.from_any(p)
+        pr.numneigh, pr.nbr, pr.disp = nn, nbr, disp
+        r = snap.run_pipeline(pr)
+        assert np.array_equal(f, r.forces) and t == r.etotal
