@@ -164,6 +164,25 @@ struct snapgpu_ctx {
 namespace snapgpu {
 namespace host {
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while the previous kernel in the stream drains; it calls pdl_wait() before
+// reading that kernel's outputs (kernels.cuh).
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 inline PairArgs pair_args(const snapgpu_ctx* c) {
   PairArgs p;
   p.nlocal = c->nlocal;

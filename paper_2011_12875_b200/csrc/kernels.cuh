@@ -168,6 +168,20 @@ __device__ __forceinline__ double neighbor_weight(const PairArgs& A, int j) {
   return A.weights[A.types ? A.types[j] : 0];
 }
 
+// Programmatic dependent launch (Hopper+ PDL, griddepcontrol): the stage
+// kernels are launched with programmatic stream serialization, so a kernel
+// starts while its predecessor drains and runs its input-independent
+// prologue (table staging, pair geometry, the forward Wigner sweep) before
+// pdl_wait(); a predecessor calls pdl_trigger() once its CTA has no more
+// work to hand out.  Without the launch attribute both are no-ops.
+// Data a predecessor writes while the dependent already runs must not go
+// through the non-coherent read-only path (ld.global.nc / __ldg): the
+// dependents read it with coherent loads (__ldca / __ldcg) after pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 // sqrt(2/t): the v-space scale between row t/2 and the mirror of row t/2-1
 // at level t-1.
 __host__ __device__ constexpr double mirror_R(int t) {
@@ -899,9 +913,10 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs
     sX[NP * 8 + e] = sX[(NP + kQPad + NF) * 8 + e] = 0.0;
   }
   const double* Vt = A.V + (size_t)(atom0 >> 5) * 2 * NH * 32 + (atom0 & 31);
+  pdl_wait();  // V comes from compute_U
   for (int e = threadIdx.x; e < NH * 8; e += blockDim.x) {
     const int h = e >> 3, a = e & 7;
-    const double re = __ldg(Vt + h * 32 + a), im = __ldg(Vt + (NH + h) * 32 + a);
+    const double re = __ldcg(Vt + h * 32 + a), im = __ldcg(Vt + (NH + h) * 32 + a);
     const int2 sc = __ldg(reinterpret_cast<const int2*>(A.expand) + h);
     sX[(kQPad + sc.x) * 8 + a] = re;
     sX[(NP + kQPad + sc.x) * 8 + a] = im;
@@ -939,6 +954,7 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs
     }
 #undef YQROW
   }
+  pdl_trigger();
   se[w][lane] = e_acc;
   __syncthreads();
   if (w == 0) {
@@ -1250,6 +1266,7 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   for (int e = threadIdx.x; e < A.nitems; e += blockDim.x) sW[e] = __ldg(A.itw + e);
   const int tile = blockIdx.x;
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
+  pdl_wait();  // V comes from compute_U
   for (int e = threadIdx.x; e < kXPad * 32; e += blockDim.x) {
     sX[e] = make_double2(0.0, 0.0);
     sX[(kXPad + NF) * 32 + e] = make_double2(0.0, 0.0);
@@ -1268,8 +1285,8 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     for (int k = 0; k < KH; ++k) {
       const int h = wq + kYWarps * k;
       if (h < NH) {
-        re[k] = __ldg(Vt + h * 32 + ln);
-        im[k] = __ldg(Vt + (NH + h) * 32 + ln);
+        re[k] = __ldcg(Vt + h * 32 + ln);
+        im[k] = __ldcg(Vt + (NH + h) * 32 + ln);
         sc[k] = __ldg(reinterpret_cast<const int2*>(A.expand) + h);
       }
     }
@@ -1325,6 +1342,7 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     t_prev = t_now;
 #endif
   }
+  pdl_trigger();  // this CTA's rows are done: let compute_dE start launching
   se[w][lane] = e_acc;
   __syncthreads();
   if (w == 0) {
@@ -1472,11 +1490,12 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
   }
   __syncwarp();
 
+  pdl_wait();  // Y' comes from compute_Y: everything above overlapped its tail
   // ---------------- backward ----------------
   // F = Re sum_t <Y'_t, v_t> telescopes through the adjoints: with
   // lambda_t = Y'_t + A_{t+1}^H lambda_{t+1} (A_t the R-linear level map),
   // F = Re <lambda_0, v_0> = Re lambda_0(0,0) since v_0 = 1.
-  double F = (T == 0 && r == 0) ? __ldg(Y2).x : 0.0;  // 2J = 0: no levels to sweep
+  double F = (T == 0 && r == 0) ? __ldca(Y2).x : 0.0;  // 2J = 0: no levels to sweep
   double Gar = 0.0, Gai = 0.0, Gbr = 0.0, Gbi = 0.0;
   double lr[C::NC], li[C::NC];  // lambda_t(r, c)
 #pragma unroll
@@ -1485,7 +1504,7 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
     const int hb = c_half_off(T) + r * (T + 1);
 #pragma unroll
     for (int c = 0; c <= T; ++c) {
-      const double2 yv = __ldg(Y2 + hb + c);
+      const double2 yv = __ldca(Y2 + hb + c);
       lr[c] = yv.x;
       li[c] = yv.y;
     }
@@ -1522,7 +1541,7 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
 #pragma unroll
       for (int c = T / 2; c >= 0; --c) {
         const double K = (((c + T / 2) & 1) ? -R : R);
-        const double2 yv = __ldg(Y2 + hb + c);
+        const double2 yv = __ldca(Y2 + hb + c);
         const double tlr = yv.x, tli = yv.y;
         const double ur = buf[(size_t)(2 * (o + T - 1 - c)) * 32];
         const double ui = buf[(size_t)(2 * (o + T - 1 - c) + 1) * 32];
@@ -1557,14 +1576,14 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
         gi_[t - 1 - c] += recv ? si_[c] : 0.0;
       }
     }
-    if (t == 1 && r == 0) F = __ldg(Y2).x + gr_[0];  // Re lambda_0(0,0)
+    if (t == 1 && r == 0) F = __ldca(Y2).x + gr_[0];  // Re lambda_0(0,0)
     // lambda_{t-1} for rows that already existed at level t-1
     if (t > 1) {
       const bool keep = 2 * r <= t - 1;
       const int hb = c_half_off(t - 1) + r * t;
 #pragma unroll
       for (int c = 0; c < t; ++c) {
-        const double2 yv = keep ? __ldg(Y2 + hb + c) : make_double2(0.0, 0.0);
+        const double2 yv = keep ? __ldca(Y2 + hb + c) : make_double2(0.0, 0.0);
         lr[c] = keep ? yv.x + gr_[c] : 0.0;
         li[c] = keep ? yv.y + gi_[c] : 0.0;
       }
@@ -1695,9 +1714,11 @@ constexpr int kGatherCap = 32;
 
 __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (A.nchunks > 1 && t < A.nchunks)
-    A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
   const int a = t / 3, d = t - 3 * (t / 3);
+  if (A.nchunks > 1 && t < A.nchunks) {  // this rank's energy into every chunk's slot
+    pdl_wait();                           // (etotal comes from compute_Y)
+    A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
+  }
   if (a >= A.pr.natoms_total) return;
   double* fo = A.forces + (size_t)(a / A.chunk_rows) * A.chunk_stride +
                (size_t)(a % A.chunk_rows) * 3 + d;
@@ -1722,6 +1743,7 @@ __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
     nn = A.pr.numneigh[il];
     nn = (nn < 0 || nn > S) ? 0 : nn;
   }
+  pdl_wait();  // dElist comes from compute_fused_dE
   double f = 0.0;
   if (nrev <= kGatherCap && nn <= kGatherCap) {
     int p[kGatherCap];

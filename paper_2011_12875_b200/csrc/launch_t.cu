@@ -114,11 +114,11 @@ void launch_Y_t(snapgpu_ctx* c) {
   if (c->y_groups == 3) {
     CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
-    k_compute_Y_cwin<T, 3><<<grid, kYWarps * 32, smem, c->stream>>>(a);
+    launch_pdl(k_compute_Y_cwin<T, 3>, grid, dim3(kYWarps * 32), smem, c->stream, a);
   } else {
     CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
-    k_compute_Y_cwin<T, 1><<<grid, kYWarps * 32, smem, c->stream>>>(a);
+    launch_pdl(k_compute_Y_cwin<T, 1>, grid, dim3(kYWarps * 32), smem, c->stream, a);
   }
   CK(cudaGetLastError());
 #else
@@ -139,7 +139,8 @@ void launch_Y_t(snapgpu_ctx* c) {
   const size_t smem = sizeof(double) * (2 * NP * 8 + (size_t)kQWarps * (T + 1) * 2 * 8);
   CK(cudaFuncSetAttribute(k_compute_Y_quad<T, kQGroups>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_compute_Y_quad<T, kQGroups><<<c->ntiles * 4, kQWarps * 32, smem, c->stream>>>(a);
+  launch_pdl(k_compute_Y_quad<T, kQGroups>, dim3(c->ntiles * 4), dim3(kQWarps * 32), smem,
+             c->stream, a);
   CK(cudaGetLastError());
 #endif
 }
@@ -180,7 +181,7 @@ void launch_DE_t(snapgpu_ctx* c) {
   if (blocks > 0) {
     CK(cudaFuncSetAttribute(k_fused_dE_rev<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             R::SMEM));
-    k_fused_dE_rev<T><<<blocks, R::WARPS * 32, R::SMEM, c->stream>>>(a);
+    launch_pdl(k_fused_dE_rev<T>, dim3(blocks), dim3(R::WARPS * 32), (size_t)R::SMEM, c->stream, a);
     CK(cudaGetLastError());
   }
 }

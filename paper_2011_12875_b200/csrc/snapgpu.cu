@@ -253,7 +253,7 @@ void launch_gather(snapgpu_ctx* c) {
   a.etotal = c->d_etotal.p;
   const int nthr = std::max(3 * c->natoms_total, c->nchunks);
   if (c->natoms_total > 0) {  // one thread per force component
-    k_gather_forces<<<(nthr + 127) / 128, 128, 0, c->stream>>>(a);
+    launch_pdl(k_gather_forces, dim3((nthr + 127) / 128), dim3(128), 0, c->stream, a);
     CK(cudaGetLastError());
   }
 }
