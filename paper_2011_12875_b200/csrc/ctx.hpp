@@ -91,17 +91,16 @@ struct snapgpu_ctx {
   std::vector<double> cg, hf, ywgt;
 
   // device tables
-  snapgpu::host::DevBuf<double> d_weights, d_cw, d_citw[2];
+  snapgpu::host::DevBuf<double> d_weights, d_cw, d_citw;
   snapgpu::host::DevBuf<int> d_tasks, d_expand;
   snapgpu::YPlan yplan;
-  snapgpu::YCoopPlan ycplan[2];  // constant-window units for 4 / 12 warps per row
+  snapgpu::YCoopPlan ycplan;     // constant-window units, LPT-split over 4 warps per row
   snapgpu::YQuadPlan yqplan;     // quad units (2J > 8)
   snapgpu::host::DevBuf<int4> d_qunits;
   snapgpu::host::DevBuf<double> d_qitw;
   snapgpu::host::DevBuf<int> d_qrw, d_qrows;
   int task_cap = 0;
   int y_parts = 0, y_parts_used = 1;  // compute_Y CTAs per 32-atom tile (0 = automatic)
-  int y_groups = 3;  // warp groups per constant-window compute_Y CTA (1 or 3)
 
   // problem shape
   int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
@@ -219,8 +218,8 @@ template <int T> void launch_DE_t(snapgpu_ctx* c);
 template <int T> void launch_B_t(snapgpu_ctx* c, double* blist);
 struct YTablesHost {  // constant-bank tables of k_compute_Y_cwin (kernels.cuh)
   std::vector<double> cw;
-  std::vector<uint4> items4, items12;
-  std::vector<int> rw4, rw12;
+  std::vector<uint4> items;
+  std::vector<int> rw;
 };
 template <int T> void upload_ytables_t(int device, const YTablesHost& t);
 #ifdef SNAP_Y_PROFILE

@@ -1089,14 +1089,15 @@ constexpr int kXPad = 12;
 #endif
 constexpr int kYWarps = SNAP_Y_WARPS;  // warps per k_compute_Y_cwin CTA
 constexpr int kMaxYParts = 8;         // CTAs per tile (row split) at most
-// A CTA runs as GR independent groups of kYWarps/GR warps: GR = 3 (large
-// problems: a group owns whole target rows, with its own row list, named
-// barrier and slice of the partial-row buffer, so rows synchronise 4 warps
-// only and the groups drift independently) or GR = 1 (small problems split
-// over several CTAs per tile: all 12 warps on one row at a time, the finest
-// row granularity).  The row-pair units of every target row are LPT-split
-// over the group's warps; each layout has its own unit table, sorted by
-// tuple within a warp so the warps of a group sweep the C' table together.
+// A CTA runs as GR = 3 independent groups of 4 warps: a group owns whole
+// target rows, with its own row list, named barrier and slice of the
+// partial-row buffer, so rows synchronise 4 warps only and the groups drift
+// independently (measured against one 12-warp group per row for tiles split
+// over several CTAs: 2000 atoms, Y 81.9 -> 75.8 us).  The row-pair units of
+// every target row are LPT-split over the group's warps, sorted by tuple
+// within a warp so the warps of a group sweep the C' table together.
+constexpr int kYGroups = 3;
+constexpr int kYGroupWarps = kYWarps / kYGroups;
 template <int GR>
 __device__ __forceinline__ void group_sync(int g) {
   if constexpr (GR == 1) {
@@ -1110,17 +1111,14 @@ constexpr int kYItemCap = 1024;  // row-pair units at 2J = 8: 838 (1479 items)
 // of the per-2J object (launch_t.cu, uploaded once per device): warp-uniform
 // reads, so every access is a broadcast from the constant cache.
 //   cCW       windowed C' coefficients, rows of length j+1 per (tuple, a2)
-//   cYItemsG  row-pair units {x1 window base (full idx + D) | x2 row base << 16,
+//   cYItems   row-pair units {x1 window base (full idx + D) | x2 row base << 16,
 //             J2 | C' offset << 8, same x1|x2 of the second item, W index},
-//             grouped by target row, then by warp (pairs, then singles), for
-//             G = 4 or 12 warps per row
-//   cYRowWG   [row][2*warp+kind] unit ranges
+//             grouped by target row, then by warp (pairs, then singles)
+//   cYRowW    [row][2*warp+kind] unit ranges
 #if defined(SNAP_T) && SNAP_T <= 8
 __constant__ double cCW[c_cw_total(SNAP_T)];
-__constant__ uint4 cYItems4[kYItemCap];
-__constant__ uint4 cYItems12[kYItemCap];
-__constant__ int cYRowW4[c_acc_off(SNAP_T + 1) * (2 * 4 + 1)];
-__constant__ int cYRowW12[c_acc_off(SNAP_T + 1) * (2 * 12 + 1)];
+__constant__ uint4 cYItems[kYItemCap];
+__constant__ int cYRowW[c_acc_off(SNAP_T + 1) * (2 * kYGroupWarps + 1)];
 #endif
 
 struct YWArgs {
@@ -1156,10 +1154,10 @@ template <int G, int L, int JW, int GW>
 __device__ __forceinline__ void yw_units(const double2* __restrict__ sX,
                                          const double* __restrict__ sW, int lane, int b, int e,
                                          double (&ar)[L], double (&ai)[L]) {
-  uint4 nxt = b < e ? ((GW == 4) ? cYItems4[b] : cYItems12[b]) : make_uint4(0u, 0u, 0u, 0u);
+  uint4 nxt = b < e ? cYItems[b] : make_uint4(0u, 0u, 0u, 0u);
   for (int it = b; it < e; ++it) {
     const uint4 m = nxt;  // the next record is in flight during this unit
-    if (it + 1 < e) nxt = (GW == 4) ? cYItems4[it + 1] : cYItems12[it + 1];
+    if (it + 1 < e) nxt = cYItems[it + 1];
     const int J2 = m.y & 0xff;
     const double* c0 = cCW + (m.y >> 8);
     const double2* p1[G];
@@ -1214,11 +1212,11 @@ __device__ __forceinline__ void yw_row(const double2* __restrict__ sX, double* _
   constexpr int L = MID ? J / 2 + 1 : J + 1;
   constexpr int JW = J + 1;
   constexpr int nw = kYWarps / GR;
-  static_assert(nw == 4 || nw == 12, "unit tables exist for 4 and 12 warps per row");
+  static_assert(nw == kYGroupWarps, "the unit table splits each row over kYGroupWarps warps");
   double ar[L], ai[L];
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
-  const int* rb = (nw == 4 ? cYRowW4 : cYRowW12) + rid * (2 * nw + 1) + 2 * w;
+  const int* rb = cYRowW + rid * (2 * nw + 1) + 2 * w;
   yw_units<2, L, JW, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
   yw_units<1, L, JW, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);  // singles
 #pragma unroll

@@ -24,13 +24,12 @@ static L2Prefetch y_prefetch(snapgpu_ctx* c) {
   {
     void* a[4] = {nullptr, nullptr, nullptr, nullptr};
     CK(cudaGetSymbolAddress(&a[0], cCW));
-    CK(cudaGetSymbolAddress(&a[1], cYItems4));
-    CK(cudaGetSymbolAddress(&a[2], cYItems12));
-    const int g = c->y_groups == 3 ? 0 : 1;
-    a[3] = c->d_citw[g].p;
-    const int b[4] = {(int)sizeof(cCW), (int)(c->ycplan[0].units.size() * sizeof(uint4)),
-                      (int)(c->ycplan[1].units.size() * sizeof(uint4)),
-                      (int)(c->ycplan[g].items.size() * sizeof(double))};
+    CK(cudaGetSymbolAddress(&a[1], cYItems));
+    CK(cudaGetSymbolAddress(&a[2], cYRowW));
+    a[3] = c->d_citw.p;
+    const int b[4] = {(int)sizeof(cCW), (int)(c->ycplan.units.size() * sizeof(uint4)),
+                      (int)(c->ycplan.rw_begin.size() * sizeof(int)),
+                      (int)(c->ycplan.items.size() * sizeof(double))};
     for (int r = 0; r < 4; ++r) {
       P.p[r] = static_cast<const char*>(a[r]);
       P.bytes[r] = a[r] ? b[r] : 0;
@@ -94,8 +93,8 @@ void launch_Y_t(snapgpu_ctx* c) {
   a.V = c->d_V.p;
   a.Y = c->d_Y.p;
   a.expand = c->d_expand.p;
-  a.itw = c->d_citw[c->y_groups == 3 ? 0 : 1].p;
-  a.nitems = static_cast<int>(c->ycplan[0].items.size());
+  a.itw = c->d_citw.p;
+  a.nitems = static_cast<int>(c->ycplan.items.size());
   a.prof = nullptr;
 #ifdef SNAP_Y_PROFILE
   if (!g_yprof) {
@@ -111,15 +110,9 @@ void launch_Y_t(snapgpu_ctx* c) {
   const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYWarps * (T + 1) * 2 * 32 +
                                         (size_t)a.nitems);
   dim3 grid(c->ntiles, c->y_parts_used);
-  if (c->y_groups == 3) {
-    CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    launch_pdl(k_compute_Y_cwin<T, 3>, grid, dim3(kYWarps * 32), smem, c->stream, a);
-  } else {
-    CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    launch_pdl(k_compute_Y_cwin<T, 1>, grid, dim3(kYWarps * 32), smem, c->stream, a);
-  }
+  CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, kYGroups>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  launch_pdl(k_compute_Y_cwin<T, kYGroups>, grid, dim3(kYWarps * 32), smem, c->stream, a);
   CK(cudaGetLastError());
 #else
   constexpr int NF = c_full_off(T + 1);
@@ -199,16 +192,12 @@ void upload_ytables_t(int device, const YTablesHost& t) {
     for (int d : done)
       if (d == device) return;
     require(t.cw.size() == (size_t)c_cw_total(T), "compute_Y: C' table size mismatch");
-    require(t.items4.size() <= (size_t)kYItemCap && t.items12.size() <= (size_t)kYItemCap,
-            "compute_Y: unit table exceeds constant bank");
-    require(t.rw4.size() == (size_t)c_acc_off(T + 1) * (2 * 4 + 1) &&
-                t.rw12.size() == (size_t)c_acc_off(T + 1) * (2 * 12 + 1),
+    require(t.items.size() <= (size_t)kYItemCap, "compute_Y: unit table exceeds constant bank");
+    require(t.rw.size() == (size_t)c_acc_off(T + 1) * (2 * kYGroupWarps + 1),
             "compute_Y: row/warp table size mismatch");
     CK(cudaMemcpyToSymbol(cCW, t.cw.data(), t.cw.size() * sizeof(double)));
-    CK(cudaMemcpyToSymbol(cYItems4, t.items4.data(), t.items4.size() * sizeof(uint4)));
-    CK(cudaMemcpyToSymbol(cYItems12, t.items12.data(), t.items12.size() * sizeof(uint4)));
-    CK(cudaMemcpyToSymbol(cYRowW4, t.rw4.data(), t.rw4.size() * sizeof(int)));
-    CK(cudaMemcpyToSymbol(cYRowW12, t.rw12.data(), t.rw12.size() * sizeof(int)));
+    CK(cudaMemcpyToSymbol(cYItems, t.items.data(), t.items.size() * sizeof(uint4)));
+    CK(cudaMemcpyToSymbol(cYRowW, t.rw.data(), t.rw.size() * sizeof(int)));
     done.push_back(device);
   }
 #else

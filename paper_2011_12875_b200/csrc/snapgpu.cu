@@ -86,12 +86,9 @@ void plan_y(snapgpu_ctx* c) {
     parts = c->y_parts;
     // one CTA per SM: never exceed a single wave
     if (parts <= 0) parts = std::max(1, std::min(kMaxYParts, nsm / std::max(1, c->ntiles)));
-    // one row list per (part, warp group): three 4-warp groups when a CTA
-    // owns a whole tile, one 12-warp group (finest row granularity) when the
-    // tile is split over several CTAs
-    c->y_groups = (parts == 1) ? 3 : 1;
+    // one row list per (part, warp group)
     std::vector<int> tasks =
-        y_row_schedule(c->maps, c->ycplan[0].row_cost, parts * c->y_groups, &c->task_cap);
+        y_row_schedule(c->maps, c->ycplan.row_cost, parts * kYGroups, &c->task_cap);
     c->d_tasks.alloc(tasks.size());
     CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
@@ -108,12 +105,9 @@ void plan_y(snapgpu_ctx* c) {
 void upload_beta(snapgpu_ctx* c) {
   const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
   if (c->T <= 8) {
-    for (int k = 0; k < 2; ++k) {  // item order of the 4- and 12-warp unit tables
-      const std::vector<double> itw = ycoop_weights(c->ycplan[k], c->maps, W);
-      c->d_citw[k].alloc(std::max<size_t>(1, itw.size()));
-      CK(cudaMemcpy(c->d_citw[k].p, itw.data(), itw.size() * sizeof(double),
-                    cudaMemcpyHostToDevice));
-    }
+    const std::vector<double> itw = ycoop_weights(c->ycplan, c->maps, W);
+    c->d_citw.alloc(std::max<size_t>(1, itw.size()));
+    CK(cudaMemcpy(c->d_citw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
     return;
   }
   const std::vector<double> itw = yquad_weights(c->yqplan, c->maps, W);
@@ -148,18 +142,14 @@ static std::vector<uint4> pack_units(const snapgpu_ctx* c, const YCoopPlan& p) {
 }
 
 void build_ycoop(snapgpu_ctx* c) {
-  c->ycplan[0] = ycoop_pair_plan(c->maps, 4);   // 4 warps per row (3 groups)
-  c->ycplan[1] = ycoop_pair_plan(c->maps, 12);  // 12 warps per row (1 group)
+  c->ycplan = ycoop_pair_plan(c->maps, kYGroupWarps);
   YTablesHost t;
   t.cw = c->yplan.cw;
-  t.items4 = pack_units(c, c->ycplan[0]);
-  t.items12 = pack_units(c, c->ycplan[1]);
-  t.rw4 = c->ycplan[0].rw_begin;
-  t.rw12 = c->ycplan[1].rw_begin;
+  t.items = pack_units(c, c->ycplan);
+  t.rw = c->ycplan.rw_begin;
   upload_ytables(c->device, c->T, t);
   upload_beta(c);
 }
-
 
 void launch_U(snapgpu_ctx* c) {
   if (c->nlocal > 0) SNAP_PICK(launch_U_t, c->T)(c);
@@ -582,7 +572,7 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_weights.release();
   c->d_cw.release();
 
-  c->d_citw[0].release();
+  c->d_citw.release();
   c->d_qunits.release();
   c->d_qitw.release();
   c->d_qrw.release();
@@ -590,7 +580,6 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_nlpos.release();
   c->d_nlint.release();
   c->d_virial.release();
-  c->d_citw[1].release();
   c->d_expand.release();
   c->d_tasks.release();
   c->d_numneigh.release();

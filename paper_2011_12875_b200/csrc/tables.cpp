@@ -360,9 +360,10 @@ YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps) {
       // measured per-row cycles of k_compute_Y_cwin (tools/yprof.py on a
       // B200, 256k atoms; the model misses the per-row and per-step
       // overheads of the small-j rows), else the FP64 instruction model.
+      // (k_compute_Y_cwin with direct x1 loads, GR = 3, 262k atoms, r02)
       static const double kMeasured8[25] = {
-          11335, 6281,  23115, 20171, 16149, 23440, 32087, 37028, 29111, 23506, 28685, 30951, 34146,
-          45839, 43764, 32435, 25296, 31193, 35644, 45185, 37471, 47032, 50489, 59654, 39880};
+          7050,  5487,  18533, 16170, 15012, 18321, 25144, 30044, 22827, 19402, 22812, 25914, 29899,
+          34546, 40189, 27725, 20532, 26596, 32257, 34000, 27325, 34365, 41883, 48782, 30904};
       const int rid = static_cast<int>(p.row_cost.size());
       p.row_cost.push_back(m.T == 8 ? kMeasured8[rid] : tot);
       std::vector<std::vector<int>> buckets = lpt(costs, warps);

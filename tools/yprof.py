@@ -3,6 +3,8 @@ import ctypes as C, sys
 import numpy as np
 sys.path.insert(0, '.')
 import paper_2011_12875_b200 as snap
+if len(sys.argv) > 1 and sys.argv[1].startswith("--lib="):  # the SNAP_Y_PROFILE build
+    snap.LIB_PATH = sys.argv.pop(1)[6:]
 
 nx, ny, nz = (int(x) for x in sys.argv[1:4])
 parts = int(sys.argv[4]) if len(sys.argv) > 4 else 0
