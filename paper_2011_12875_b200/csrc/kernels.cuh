@@ -1410,12 +1410,18 @@ struct DERCfg {
   static constexpr int NC = T + 1;
   static constexpr int NH = c_half_off(T + 1);
   static constexpr int NIN = T * (T + 1) / 2 > 0 ? T * (T + 1) / 2 : 1;  // inputs of row 0
+#ifndef SNAP_DE_WARPS
   static constexpr int WARPS = (NIN * 2 * 32 * 8 * 4 <= 80 * 1024) ? 4 : 2;
+#else
+  static constexpr int WARPS = SNAP_DE_WARPS;
+#endif
   static constexpr int SMEM = WARPS * NIN * 2 * 32 * 8;
+  // CTAs per SM: 12 warps (register bound) at 2J <= 8
+  static constexpr int MINB = T <= 8 ? 12 / WARPS : 1;
 };
 
 template <int T>
-__global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
+__global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
     k_fused_dE_rev(const DEArgs A) {
   using C = DERCfg<T>;
   if (pipeline_failed(A.pr)) return;
@@ -1494,7 +1500,9 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
   // lambda_t = Y'_t + A_{t+1}^H lambda_{t+1} (A_t the R-linear level map),
   // F = Re <lambda_0, v_0> = Re lambda_0(0,0) since v_0 = 1.
   double F = (T == 0 && r == 0) ? __ldca(Y2).x : 0.0;  // 2J = 0: no levels to sweep
-  double Gar = 0.0, Gai = 0.0, Gbr = 0.0, Gbi = 0.0;
+  // parameter gradients, split by column parity: two independent FMA chains
+  // each (the gradient sums otherwise serialise the sweep)
+  double Gar[2] = {0.0, 0.0}, Gai[2] = {0.0, 0.0}, Gbr[2] = {0.0, 0.0}, Gbi[2] = {0.0, 0.0};
   double lr[C::NC], li[C::NC];  // lambda_t(r, c)
 #pragma unroll
   for (int c = 0; c < C::NC; ++c) lr[c] = li[c] = 0.0;
@@ -1521,10 +1529,11 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
         const double pr = buf[(size_t)(2 * (o + c)) * 32];
         const double pi = buf[(size_t)(2 * (o + c) + 1) * 32];
         // input P(c) feeds element c (coefficient conj a) and c+1 (-conj b)
-        Gar += lr[c] * pr + li[c] * pi;
-        Gai += lr[c] * pi - li[c] * pr;
-        Gbr -= lr[c + 1] * pr + li[c + 1] * pi;
-        Gbi -= lr[c + 1] * pi - li[c + 1] * pr;
+        const int h = c & 1;
+        Gar[h] = fma(li[c], pi, fma(lr[c], pr, Gar[h]));
+        Gai[h] = fma(-li[c], pr, fma(lr[c], pi, Gai[h]));
+        Gbr[h] = fma(-li[c + 1], pi, fma(-lr[c + 1], pr, Gbr[h]));
+        Gbi[h] = fma(li[c + 1], pr, fma(-lr[c + 1], pi, Gbi[h]));
         gr_[c] = ar * lr[c] - ai * li[c] - br * lr[c + 1] + bi * li[c + 1];
         gi_[c] = ar * li[c] + ai * lr[c] - br * li[c + 1] - bi * lr[c + 1];
       }
@@ -1544,10 +1553,11 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
         const double ur = buf[(size_t)(2 * (o + T - 1 - c)) * 32];
         const double ui = buf[(size_t)(2 * (o + T - 1 - c) + 1) * 32];
         const double pr = K * ur, pi = -K * ui;  // pm(c)
-        Gar += tlr * pr + tli * pi;
-        Gai += tlr * pi - tli * pr;
-        Gbr -= nlr * pr + nli * pi;
-        Gbi -= nlr * pi - nli * pr;
+        const int h = c & 1;
+        Gar[h] = fma(tli, pi, fma(tlr, pr, Gar[h]));
+        Gai[h] = fma(-tli, pr, fma(tlr, pi, Gai[h]));
+        Gbr[h] = fma(-nli, pi, fma(-nlr, pr, Gbr[h]));
+        Gbi[h] = fma(nli, pr, fma(-nlr, pi, Gbi[h]));
         const double gr = ar * tlr - ai * tli - br * nlr + bi * nli;
         const double gi = ar * tli + ai * tlr - br * nli - bi * nlr;
         gr_[T - 1 - c] += K * gr;  // conj, times K
@@ -1589,20 +1599,22 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, (T <= 8 ? 3 : 1))
     }
   }
   // reduce the row-lanes of the pair
+  double gar = Gar[0] + Gar[1], gai = Gai[0] + Gai[1], gbr = Gbr[0] + Gbr[1],
+         gbi = Gbi[0] + Gbi[1];
 #pragma unroll
   for (int o = 1; o < C::G; o <<= 1) {
     F += __shfl_xor_sync(0xffffffffu, F, o);
-    Gar += __shfl_xor_sync(0xffffffffu, Gar, o);
-    Gai += __shfl_xor_sync(0xffffffffu, Gai, o);
-    Gbr += __shfl_xor_sync(0xffffffffu, Gbr, o);
-    Gbi += __shfl_xor_sync(0xffffffffu, Gbi, o);
+    gar += __shfl_xor_sync(0xffffffffu, gar, o);
+    gai += __shfl_xor_sync(0xffffffffu, gai, o);
+    gbr += __shfl_xor_sync(0xffffffffu, gbr, o);
+    gbi += __shfl_xor_sync(0xffffffffu, gbi, o);
   }
   if (valid && r == 0) {
     double* o = A.dedr + (size_t)p * 3;
     double de[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const double dF = Gar * g.dar[d] + Gai * g.dai[d] + Gbr * g.dbr[d] + Gbi * g.dbi[d];
+      const double dF = gar * g.dar[d] + gai * g.dai[d] + gbr * g.dbr[d] + gbi * g.dbi[d];
       de[d] = 2.0 * (g.dsf[d] * F + g.sfac * dF);
       o[d] = de[d];
     }
