@@ -182,6 +182,12 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+// 1/sqrt(m!): the v-space self term wself f(t,m,m) on the diagonal (warp-
+// uniform index in the row-lane U kernel: a constant-bank read)
+__constant__ double kInvSqrtFact[8] = {1.0, 1.0, 0.70710678118654752440, 0.40824829046386301637,
+                                       0.20412414523193150819, 0.091287092917527685576,
+                                       0.037267799624996494940, 0.014085904245475275327};
+
 // sqrt(2/t): the v-space scale between row t/2 and the mirror of row t/2-1
 // at level t-1.
 __host__ __device__ constexpr double mirror_R(int t) {
@@ -542,9 +548,15 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
 #pragma unroll
   for (int q = 0; q < C::NACC; ++q) accr[q] = acci[q] = 0.0;
   constexpr int NM = (T & 1) == 0 ? T / 2 + 1 : 1;  // transient last middle row
-  double amr[NM], ami[NM];
+  // The lane producing it (row T/2-1) has no row at levels < T-2, so from
+  // 2J = 4 on its accumulator slots of those levels hold the transient row
+  // (fewer registers); 2J = 2 keeps separate ones.
+  constexpr bool FOLD = (T & 1) == 0 && T >= 4;
+  static_assert(!FOLD || (T - 2) * (T - 1) / 2 >= NM, "free slots for the transient row");
+  constexpr int NMR = FOLD ? 1 : NM;
+  double amr[NMR], ami[NMR];
 #pragma unroll
-  for (int q = 0; q < NM; ++q) amr[q] = ami[q] = 0.0;
+  for (int q = 0; q < NMR; ++q) amr[q] = ami[q] = 0.0;
 
   for (int p = 0; p < passes; ++p) {
     // PP pairs per lane per pass: independent recursions interleaved (ILP),
@@ -601,8 +613,13 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
             const double pr = K * vr[pp][T - 1 - c], pi = -K * vi[pp][T - 1 - c];
             const double nr = ar[pp] * pr + ai[pp] * pi - br[pp] * plr - bi[pp] * pli;
             const double ni = ar[pp] * pi - ai[pp] * pr - br[pp] * pli + bi[pp] * plr;
-            amr[c] = fma(sf[pp], nr, amr[c]);
-            ami[c] = fma(sf[pp], ni, ami[c]);
+            if constexpr (FOLD) {
+              accr[c] = fma(sf[pp], nr, accr[c]);
+              acci[c] = fma(sf[pp], ni, acci[c]);
+            } else {
+              amr[c] = fma(sf[pp], nr, amr[c]);
+              ami[c] = fma(sf[pp], ni, ami[c]);
+            }
             plr = pr;
             pli = pi;
           }
@@ -635,15 +652,12 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
       acci[q] += __shfl_xor_sync(0xffffffffu, acci[q], o);
     }
 #pragma unroll
-    for (int q = 0; q < NM; ++q) {
+    for (int q = 0; q < (FOLD ? 0 : NMR); ++q) {
       amr[q] += __shfl_xor_sync(0xffffffffu, amr[q], o);
       ami[q] += __shfl_xor_sync(0xffffffffu, ami[q], o);
     }
   }
   if (s != 0 || r >= C::NL || i >= A.pr.nlocal) return;
-  const double inv_sqrt_fact[8] = {1.0, 1.0, 0.70710678118654752440, 0.40824829046386301637,
-                                   0.20412414523193150819, 0.091287092917527685576,
-                                   0.037267799624996494940, 0.014085904245475275327};
   const double self = A.gp.self_flag ? A.gp.wself : 0.0;
   double* Vr = A.V + ((size_t)(i >> 5) * 2 * C::NH) * 32 + (i & 31);
   double* Vi = Vr + (size_t)C::NH * 32;
@@ -653,7 +667,7 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
 #pragma unroll
     for (int c = 0; c <= t; ++c) {
       double vr_ = accr[t * (t + 1) / 2 + c];
-      if (c == r) vr_ += self * inv_sqrt_fact[r];  // wself * f(t,mb,mb) (snap_core.hpp:404-413)
+      if (c == r) vr_ += self * kInvSqrtFact[r];  // wself * f(t,mb,mb) (snap_core.hpp:404-413)
       const int h = c_half_off(t) + r * (t + 1) + c;
       Vr[(size_t)h * 32] = vr_;
       Vi[(size_t)h * 32] = acci[t * (t + 1) / 2 + c];
@@ -665,14 +679,15 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
     const int hb = c_half_off(T) + (T / 2) * (T + 1);
 #pragma unroll
     for (int c = 0; c <= T / 2; ++c) {
-      double mr = amr[c];
-      if (c == T / 2) mr += self * inv_sqrt_fact[T / 2];
+      double mr = FOLD ? accr[c] : amr[c];
+      const double mi = FOLD ? acci[c] : ami[c];
+      if (c == T / 2) mr += self * kInvSqrtFact[T / 2];
       Vr[(size_t)(hb + c) * 32] = mr;
-      Vi[(size_t)(hb + c) * 32] = ami[c];
+      Vi[(size_t)(hb + c) * 32] = mi;
       if (c < T / 2) {
         const double sg = ((c + T / 2) & 1) ? -1.0 : 1.0;
         Vr[(size_t)(hb + T - c) * 32] = sg * mr;
-        Vi[(size_t)(hb + T - c) * 32] = -sg * ami[c];
+        Vi[(size_t)(hb + T - c) * 32] = -sg * mi;
       }
     }
   }
