@@ -91,7 +91,10 @@ struct snapgpu_ctx {
   std::vector<double> cg, hf, ywgt;
 
   // device tables
-  snapgpu::host::DevBuf<double> d_weights, d_cw, d_citw;
+  snapgpu::host::DevBuf<double> d_weights, d_cw;
+  snapgpu::host::DevBuf<double> d_cwp;    // padded windowed C' of k_compute_Y_cwin
+  snapgpu::host::DevBuf<uint4> d_yunits;  // its unit records (YUnit: 2 x uint4, W included)
+  std::vector<uint4> yunit_rec;           // beta-independent half of the records
   snapgpu::host::DevBuf<int> d_tasks, d_expand;
   snapgpu::YPlan yplan;
   snapgpu::YCoopPlan ycplan;     // constant-window units, LPT-split over 4 warps per row
@@ -217,8 +220,6 @@ template <int T> void launch_Y_t(snapgpu_ctx* c);
 template <int T> void launch_DE_t(snapgpu_ctx* c);
 template <int T> void launch_B_t(snapgpu_ctx* c, double* blist);
 struct YTablesHost {  // constant-bank tables of k_compute_Y_cwin (kernels.cuh)
-  std::vector<double> cw;
-  std::vector<uint4> items;
   std::vector<int> rw;
 };
 template <int T> void upload_ytables_t(int device, const YTablesHost& t);

@@ -1083,22 +1083,13 @@ __global__ void __launch_bounds__(384, 1) k_compute_B(const BArgs A) {
 // in shared memory; each warp finishes a stripe of outputs.  The code is a
 // handful of small loops, so the SM's instruction caches hold it.
 // ===========================================================================
-__host__ __device__ constexpr int c_cw_total(int T) {
-  int o = 0;
-  for (int j1 = 0; j1 <= T; ++j1)
-    for (int j2 = 0; j2 <= j1; ++j2)
-      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) o += (j2 + 1) * (j + 1);
-  return o;
-}
-__host__ __device__ constexpr int cw_base(int T) {  // windowed C' of 2J = 0..8 stacked
-  if (T > 8) return -1;
-  int o = 0;
-  for (int s = 0; s < T; ++s) o += c_cw_total(s);
-  return o;
-}
 // X planes carry kXPad zero elements on each side: the window reads reach
 // kXPad >= J2 + 1 = 9 below the first row and D <= 8 above the last.
 constexpr int kXPad = 12;
+// band limits served by k_compute_Y_cwin (the rest: k_compute_Y_quad)
+#ifndef SNAP_CWIN_MAXT
+#define SNAP_CWIN_MAXT 8
+#endif
 #ifndef SNAP_Y_WARPS
 #define SNAP_Y_WARPS 12
 #endif
@@ -1111,8 +1102,12 @@ constexpr int kMaxYParts = 8;         // CTAs per tile (row split) at most
 // over several CTAs: 2000 atoms, Y 81.9 -> 75.8 us).  The row-pair units of
 // every target row are LPT-split over the group's warps, sorted by tuple
 // within a warp so the warps of a group sweep the C' table together.
-constexpr int kYGroups = 3;
-constexpr int kYGroupWarps = kYWarps / kYGroups;
+constexpr int kYGroupWarps = 4;
+constexpr int kYGroups = kYWarps / kYGroupWarps;
+static_assert(kYGroups * kYGroupWarps == kYWarps, "whole warp groups");
+// partial-row slots: warp 0 of a group keeps its partial row in registers and
+// finishes the row; the other warps of the group store theirs
+constexpr int kYRedSlots = kYGroups * (kYGroupWarps - 1);
 template <int GR>
 __device__ __forceinline__ void group_sync(int g) {
   if constexpr (GR == 1) {
@@ -1121,18 +1116,28 @@ __device__ __forceinline__ void group_sync(int g) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"((kYWarps / GR) * 32) : "memory");
   }
 }
-constexpr int kYItemCap = 1024;  // row-pair units at 2J = 8: 838 (1479 items)
-// beta-independent tables of the constant-window kernel, in the constant bank
-// of the per-2J object (launch_t.cu, uploaded once per device): warp-uniform
-// reads, so every access is a broadcast from the constant cache.
-//   cCW       windowed C' coefficients, rows of length j+1 per (tuple, a2)
-//   cYItems   row-pair units {x1 window base (full idx + D) | x2 row base << 16,
-//             J2 | C' offset << 8, same x1|x2 of the second item, W index},
-//             grouped by target row, then by warp (pairs, then singles)
-//   cYRowW    [row][2*warp+kind] unit ranges
-#if defined(SNAP_T) && SNAP_T <= 8
-__constant__ double cCW[c_cw_total(SNAP_T)];
-__constant__ uint4 cYItems[kYItemCap];
+// Row-pair units of the constant-window kernel at 2J = 8: 838 (1479 items).
+// A unit record (global, per context, read with warp-uniform __ldg one unit
+// ahead): {x1 window base (full idx + D) | x2 row base << 16, J2 | C' offset
+// << 8, same x1|x2 of the second item, 0} and the W of its items (beta-
+// dependent).  The records are grouped by target row, then by warp (pairs,
+// then singles); cYRowW[row][2*warp+kind] holds the unit ranges (beta-
+// independent, in the constant bank of the per-2J object).
+// The windowed C' coefficients are staged into shared memory per CTA, rows
+// padded to even length so two coefficients are one 16-byte broadcast load.
+struct YUnit {
+  uint4 m;
+  double2 w;
+};
+__host__ __device__ constexpr int cw_row(int j) { return (j + 2) & ~1; }  // padded C' row
+__host__ __device__ constexpr int c_cwp_total(int T) {
+  int o = 0;
+  for (int j1 = 0; j1 <= T; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int j = j1 - j2; j <= (j1 + j2 < T ? j1 + j2 : T); j += 2) o += (j2 + 1) * cw_row(j);
+  return o;
+}
+#if defined(SNAP_T) && SNAP_T <= SNAP_CWIN_MAXT
 __constant__ int cYRowW[c_acc_off(SNAP_T + 1) * (2 * kYGroupWarps + 1)];
 #endif
 
@@ -1140,8 +1145,8 @@ struct YWArgs {
   const double* V;
   double* Y;
   const int* expand;    // half -> full scatter map (tables.cpp:half_scatter_map)
-  const double* itw;    // W per item (beta-dependent; staged into shared memory)
-  int nitems;
+  const YUnit* units;   // unit records + W
+  const double* cw;     // padded windowed C' (staged into shared memory)
   long long* prof;      // SNAP_Y_PROFILE builds: per-row cycle sums (else unused)
   const int* tasks;
   int task_cap;
@@ -1149,7 +1154,7 @@ struct YWArgs {
   EnergyOut E;
 };
 
-#if defined(SNAP_T) && SNAP_T <= 8
+#if defined(SNAP_T) && SNAP_T <= SNAP_CWIN_MAXT
 
 // G row-pair items (G = 1, or a pair of items sharing tuple and target row,
 // hence every C' coefficient) accumulated into the row outputs acc[ma]:
@@ -1159,22 +1164,35 @@ struct YWArgs {
 // window aligned with the outputs would load one element per step instead,
 // but re-aligning it costs 2(L-1) register moves per item and step and ~1.5x
 // the registers; measured on B200 the direct loads win (2000 atoms: Y 92 ->
-// 84 us; 262k atoms 7.61 -> 7.06 ms), shared-memory bandwidth has headroom.
+// 84 us; 262k atoms 7.61 -> 7.06 ms).  Within an unrolled block of U steps
+// the compiler loads each x1 element once (L + U - 1 loads per item instead
+// of U L); U = 3 measured best with C' in shared memory (262k atoms: U = 2 /
+// 3 / 4 -> 6.70 / 6.38 / 6.30 ms, 2000 atoms 71.7 / 71.7 / 73.7 us).
 #ifndef SNAP_Y_UNROLL
-#define SNAP_Y_UNROLL 2
+#define SNAP_Y_UNROLL 3
 #endif
-constexpr int kYUnroll = SNAP_Y_UNROLL;  // a2 steps unrolled (loads of the next step overlap)
+constexpr int kYUnroll = SNAP_Y_UNROLL;  // a2 steps unrolled (x1 loads shared across the block)
 
-template <int G, int L, int JW, int GW>
+__device__ __forceinline__ YUnit load_unit(const YUnit* u) {
+  YUnit r;
+  r.m = __ldg(reinterpret_cast<const uint4*>(u));
+  r.w = __ldg(reinterpret_cast<const double2*>(u) + 1);
+  return r;
+}
+
+template <int G, int L, int JWP>
 __device__ __forceinline__ void yw_units(const double2* __restrict__ sX,
-                                         const double* __restrict__ sW, int lane, int b, int e,
+                                         const double* __restrict__ sC,
+                                         const YUnit* __restrict__ units, int lane, int b, int e,
                                          double (&ar)[L], double (&ai)[L]) {
-  uint4 nxt = b < e ? cYItems[b] : make_uint4(0u, 0u, 0u, 0u);
+  YUnit nxt{};
+  if (b < e) nxt = load_unit(units + b);
   for (int it = b; it < e; ++it) {
-    const uint4 m = nxt;  // the next record is in flight during this unit
-    if (it + 1 < e) nxt = cYItems[it + 1];
+    const YUnit u = nxt;  // the next record is in flight during this unit
+    if (it + 1 < e) nxt = load_unit(units + it + 1);
+    const uint4 m = u.m;
     const int J2 = m.y & 0xff;
-    const double* c0 = cCW + (m.y >> 8);
+    const double* c0 = sC + (m.y >> 8);
     const double2* p1[G];
     const double2* p2[G];
     double wt[G];
@@ -1183,7 +1201,7 @@ __device__ __forceinline__ void yw_units(const double2* __restrict__ sX,
       const unsigned xb = g == 0 ? m.x : m.z;
       p1[g] = sX + (kXPad + (int)(xb & 0xffff)) * 32 + lane;  // x1[base + k] at p1[k * 32]
       p2[g] = sX + (kXPad + (int)(xb >> 16)) * 32 + lane;
-      wt[g] = sW[m.w + g];
+      wt[g] = g == 0 ? u.w.x : u.w.y;
     }
 #pragma unroll kYUnroll
     for (int a2 = 0; a2 <= J2; ++a2) {
@@ -1194,10 +1212,11 @@ __device__ __forceinline__ void yw_units(const double2* __restrict__ sX,
         x2r[g] = wt[g] * v.x;
         x2i[g] = wt[g] * v.y;
       }
-      const double* c = c0 + a2 * JW;
+      const double2* c = reinterpret_cast<const double2*>(c0 + a2 * JWP);
 #pragma unroll
       for (int ma = 0; ma < L; ++ma) {
-        const double cc = c[ma];
+        const double2 cp = c[ma >> 1];  // broadcast: every lane reads the same pair
+        const double cc = (ma & 1) ? cp.y : cp.x;
         const double2 x1 = p1[0][(ma - a2) * 32];
         double pr = x1.x * x2r[0];
         double pi = x1.x * x2i[0];
@@ -1220,42 +1239,50 @@ __device__ __forceinline__ void yw_units(const double2* __restrict__ sX,
 
 template <int T, int J, bool MID, int GR>
 __device__ __forceinline__ void yw_row(const double2* __restrict__ sX, double* __restrict__ sred,
-                                       const double* __restrict__ sW,
+                                       const double* __restrict__ sC,
                                        int lane, int g, int w, int mb, int rid, const YWArgs& A,
                                        double* __restrict__ Yt, double& e_acc) {
   // g = group, w = warp within the group; sred = the group's slice
   constexpr int L = MID ? J / 2 + 1 : J + 1;
-  constexpr int JW = J + 1;
+  constexpr int JWP = cw_row(J);
   constexpr int nw = kYWarps / GR;
   static_assert(nw == kYGroupWarps, "the unit table splits each row over kYGroupWarps warps");
   double ar[L], ai[L];
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
   const int* rb = cYRowW + rid * (2 * nw + 1) + 2 * w;
-  yw_units<2, L, JW, nw>(sX, sW, lane, rb[0], rb[1], ar, ai);  // pairs
-  yw_units<1, L, JW, nw>(sX, sW, lane, rb[1], rb[2], ar, ai);  // singles
+  yw_units<2, L, JWP>(sX, sC, A.units, lane, rb[0], rb[1], ar, ai);  // pairs
+  yw_units<1, L, JWP>(sX, sC, A.units, lane, rb[1], rb[2], ar, ai);  // singles
+  if (w > 0) {
 #pragma unroll
-  for (int m = 0; m < L; ++m) {
-    sred[((w * (T + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
-    sred[((w * (T + 1) + m) * 2 + 1) * 32 + lane] = ai[m];
+    for (int m = 0; m < L; ++m) {
+      sred[(((w - 1) * (T + 1) + m) * 2 + 0) * 32 + lane] = ar[m];
+      sred[(((w - 1) * (T + 1) + m) * 2 + 1) * 32 + lane] = ai[m];
+    }
   }
   group_sync<GR>(g);
-  const int hb = c_half_off(J) + mb * (J + 1);
-  const int fb = kXPad + c_full_off(J) + mb * (J + 1);
-  for (int ma = w; ma <= J; ma += nw) {
-    double yr = 0.0, yi = 0.0;
-    if (ma < L) {
-      for (int q = 0; q < nw; ++q) {
-        yr += sred[((q * (T + 1) + ma) * 2 + 0) * 32 + lane];
-        yi += sred[((q * (T + 1) + ma) * 2 + 1) * 32 + lane];
+  if (w == 0) {  // fixed summation order: own partial, then warps 1..nw-1
+    const int hb = c_half_off(J) + mb * (J + 1);
+    const int fb = kXPad + c_full_off(J) + mb * (J + 1);
+#pragma unroll
+    for (int ma = 0; ma <= J; ++ma) {
+      double yr = 0.0, yi = 0.0;
+      if (ma < L) {
+        yr = ar[ma];
+        yi = ai[ma];
+#pragma unroll
+        for (int q = 0; q < nw - 1; ++q) {
+          yr += sred[((q * (T + 1) + ma) * 2 + 0) * 32 + lane];
+          yi += sred[((q * (T + 1) + ma) * 2 + 1) * 32 + lane];
+        }
+        const double wgt = (MID && 2 * ma == J) ? 0.5 : 1.0;
+        yr *= wgt;
+        yi *= wgt;
+        const double2 x = sX[(fb + ma) * 32 + lane];
+        e_acc += yr * x.x + yi * x.y;
       }
-      const double wgt = (MID && 2 * ma == J) ? 0.5 : 1.0;
-      yr *= wgt;
-      yi *= wgt;
-      const double2 x = sX[(fb + ma) * 32 + lane];
-      e_acc += yr * x.x + yi * x.y;
+      reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
     }
-    reinterpret_cast<double2*>(Yt)[hb + ma] = make_double2(yr, yi);
   }
   group_sync<GR>(g);
 }
@@ -1269,14 +1296,15 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   extern __shared__ double smem[];
   double2* sX = reinterpret_cast<double2*>(smem);  // [pad | full idx | pad][32] (re, im)
   double* sred = smem + 2 * NP * 32;               // [warp][T+1][re|im][32]
-  double* sW = sred + kYWarps * (T + 1) * 2 * 32;  // W per item
+  double* sC = sred + kYRedSlots * (T + 1) * 2 * 32;  // padded windowed C'
   __shared__ double se[kYWarps][32];
 #ifdef SNAP_Y_PROFILE
   const long long t_start = clock64();
   unsigned long long g_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 #endif
-  for (int e = threadIdx.x; e < A.nitems; e += blockDim.x) sW[e] = __ldg(A.itw + e);
+  for (int e = threadIdx.x; e < c_cwp_total(T) / 2; e += blockDim.x)
+    reinterpret_cast<double2*>(sC)[e] = __ldg(reinterpret_cast<const double2*>(A.cw) + e);
   const int tile = blockIdx.x;
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
   pdl_wait();  // V comes from compute_U
@@ -1320,7 +1348,7 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = w / kYGW, wg = w - g * kYGW;
   const int* tasks = A.tasks + (size_t)(blockIdx.y * GR + g) * A.task_cap;
-  double* sredg = sred + (size_t)g * kYGW * (T + 1) * 2 * 32;
+  double* sredg = sred + (size_t)g * (kYGW - 1) * (T + 1) * 2 * 32;
   double* Yt = A.Y + (size_t)(tile * 32 + lane) * NH * 2;  // Y' atom-major, interleaved complex
   double e_acc = 0.0;
 #ifdef SNAP_Y_PROFILE
@@ -1339,8 +1367,8 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
 #define YWROW(JJ)                                                                       \
   case JJ:                                                                              \
     if constexpr (JJ <= T) {                                                            \
-      if (2 * mb == JJ) yw_row<T, JJ, true, GR>(sX, sredg, sW, lane, g, wg, mb, rid, A, Yt, e_acc); \
-      else yw_row<T, JJ, false, GR>(sX, sredg, sW, lane, g, wg, mb, rid, A, Yt, e_acc);          \
+      if (2 * mb == JJ) yw_row<T, JJ, true, GR>(sX, sredg, sC, lane, g, wg, mb, rid, A, Yt, e_acc); \
+      else yw_row<T, JJ, false, GR>(sX, sredg, sC, lane, g, wg, mb, rid, A, Yt, e_acc);          \
     }                                                                                   \
     break;
     switch (j) {

@@ -20,17 +20,15 @@ namespace host {
 template <int T>
 static L2Prefetch y_prefetch(snapgpu_ctx* c) {
   L2Prefetch P{};
-#if SNAP_T <= 8
+#if SNAP_T <= SNAP_CWIN_MAXT
   {
-    void* a[4] = {nullptr, nullptr, nullptr, nullptr};
-    CK(cudaGetSymbolAddress(&a[0], cCW));
-    CK(cudaGetSymbolAddress(&a[1], cYItems));
-    CK(cudaGetSymbolAddress(&a[2], cYRowW));
-    a[3] = c->d_citw.p;
-    const int b[4] = {(int)sizeof(cCW), (int)(c->ycplan.units.size() * sizeof(uint4)),
-                      (int)(c->ycplan.rw_begin.size() * sizeof(int)),
-                      (int)(c->ycplan.items.size() * sizeof(double))};
-    for (int r = 0; r < 4; ++r) {
+    void* rw = nullptr;
+    CK(cudaGetSymbolAddress(&rw, cYRowW));
+    const void* a[3] = {c->d_yunits.p, c->d_cwp.p, rw};
+    const int b[3] = {(int)(c->ycplan.units.size() * sizeof(YUnit)),
+                      (int)(c_cwp_total(T) * sizeof(double)),
+                      (int)(c->ycplan.rw_begin.size() * sizeof(int))};
+    for (int r = 0; r < 3; ++r) {
       P.p[r] = static_cast<const char*>(a[r]);
       P.bytes[r] = a[r] ? b[r] : 0;
     }
@@ -86,15 +84,15 @@ void launch_U_t(snapgpu_ctx* c) {
 
 template <int T>
 void launch_Y_t(snapgpu_ctx* c) {
-#if SNAP_T <= 8
+#if SNAP_T <= SNAP_CWIN_MAXT
   constexpr int NF = c_full_off(T + 1);
   constexpr int NP = NF + 2 * kXPad;
   YWArgs a;
   a.V = c->d_V.p;
   a.Y = c->d_Y.p;
   a.expand = c->d_expand.p;
-  a.itw = c->d_citw.p;
-  a.nitems = static_cast<int>(c->ycplan.items.size());
+  a.units = reinterpret_cast<const YUnit*>(c->d_yunits.p);
+  a.cw = c->d_cwp.p;
   a.prof = nullptr;
 #ifdef SNAP_Y_PROFILE
   if (!g_yprof) {
@@ -107,8 +105,8 @@ void launch_Y_t(snapgpu_ctx* c) {
   a.task_cap = c->task_cap;
   a.nlocal = c->nlocal;
   a.E = energy_out(c);
-  const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYWarps * (T + 1) * 2 * 32 +
-                                        (size_t)a.nitems);
+  const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYRedSlots * (T + 1) * 2 * 32 +
+                                        (size_t)c_cwp_total(T));
   dim3 grid(c->ntiles, c->y_parts_used);
   CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, kYGroups>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -179,24 +177,20 @@ void launch_DE_t(snapgpu_ctx* c) {
   }
 }
 
-// The beta-independent tables of the constant-window compute_Y (windowed C',
-// packed row-pair items, [row][warp] ranges) live in this object's constant
-// bank (kernels.cuh), uploaded once per device.
+// The beta-independent [row][warp] unit ranges of the constant-window
+// compute_Y live in this object's constant bank (kernels.cuh), uploaded once
+// per device.
 template <int T>
 void upload_ytables_t(int device, const YTablesHost& t) {
-#if SNAP_T <= 8
+#if SNAP_T <= SNAP_CWIN_MAXT
   {
     static std::mutex mu;
     static std::vector<int> done;
     std::lock_guard<std::mutex> lk(mu);
     for (int d : done)
       if (d == device) return;
-    require(t.cw.size() == (size_t)c_cw_total(T), "compute_Y: C' table size mismatch");
-    require(t.items.size() <= (size_t)kYItemCap, "compute_Y: unit table exceeds constant bank");
     require(t.rw.size() == (size_t)c_acc_off(T + 1) * (2 * kYGroupWarps + 1),
             "compute_Y: row/warp table size mismatch");
-    CK(cudaMemcpyToSymbol(cCW, t.cw.data(), t.cw.size() * sizeof(double)));
-    CK(cudaMemcpyToSymbol(cYItems, t.items.data(), t.items.size() * sizeof(uint4)));
     CK(cudaMemcpyToSymbol(cYRowW, t.rw.data(), t.rw.size() * sizeof(int)));
     done.push_back(device);
   }

@@ -80,7 +80,7 @@ void build_ycoop(snapgpu_ctx* c);
 
 void plan_y(snapgpu_ctx* c) {
   int parts = 1;
-  if (c->T <= 8) {
+  if (c->T <= SNAP_CWIN_MAXT) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
     parts = c->y_parts;
@@ -104,10 +104,18 @@ void plan_y(snapgpu_ctx* c) {
 
 void upload_beta(snapgpu_ctx* c) {
   const std::vector<double> W = w_table(c->maps, c->cg, c->beta.data(), false);
-  if (c->T <= 8) {
+  if (c->T <= SNAP_CWIN_MAXT) {
+    // unit records: the beta-independent half + the W of the unit's items
     const std::vector<double> itw = ycoop_weights(c->ycplan, c->maps, W);
-    c->d_citw.alloc(std::max<size_t>(1, itw.size()));
-    CK(cudaMemcpy(c->d_citw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
+    const size_t nu = c->ycplan.units.size();
+    std::vector<YUnit> u(nu);
+    for (size_t q = 0; q < nu; ++q) {
+      const int i0 = c->ycplan.units[q][0], n = c->ycplan.units[q][1];
+      u[q].m = c->yunit_rec[q];
+      u[q].w = make_double2(itw[i0], n == 2 ? itw[i0 + 1] : 0.0);
+    }
+    c->d_yunits.alloc(std::max<size_t>(1, 2 * nu));
+    CK(cudaMemcpy(c->d_yunits.p, u.data(), nu * sizeof(YUnit), cudaMemcpyHostToDevice));
     return;
   }
   const std::vector<double> itw = yquad_weights(c->yqplan, c->maps, W);
@@ -115,13 +123,14 @@ void upload_beta(snapgpu_ctx* c) {
   CK(cudaMemcpy(c->d_qitw.p, itw.data(), itw.size() * sizeof(double), cudaMemcpyHostToDevice));
 }
 
-// constant-window units, packed for the constant bank (kernels.cuh cYItems4/12)
+// constant-window units (kernels.cuh YUnit): the beta-independent record
+// half; C' offsets index the padded windowed table (rows of cw_row(j))
 static std::vector<uint4> pack_units(const snapgpu_ctx* c, const YCoopPlan& p) {
   std::vector<int> cwoff(c->maps.tuples.size());
   int o = 0;
   for (size_t q = 0; q < cwoff.size(); ++q) {
     cwoff[q] = o;
-    o += (c->maps.tuples[q].j2 + 1) * (c->maps.tuples[q].j + 1);
+    o += (c->maps.tuples[q].j2 + 1) * cw_row(c->maps.tuples[q].j);
   }
   auto rows = [&](int i) {  // x1 window base | x2 row base << 16 of item i
     const Tuple& tp = c->maps.tuples[p.items[i][0]];
@@ -136,16 +145,32 @@ static std::vector<uint4> pack_units(const snapgpu_ctx* c, const YCoopPlan& p) {
     const int i0 = p.units[u][0], n = p.units[u][1];
     const Tuple& tp = c->maps.tuples[p.items[i0][0]];
     out[u] = make_uint4(rows(i0), tp.j2 | (cwoff[p.items[i0][0]] << 8),
-                        rows(n == 2 ? i0 + 1 : i0), static_cast<unsigned>(i0));
+                        rows(n == 2 ? i0 + 1 : i0), 0u);
   }
+  return out;
+}
+
+// y_plan's windowed C' (per tuple (j2+1) rows of j+1) with rows padded to
+// cw_row(j) doubles (16-byte aligned coefficient pairs)
+static std::vector<double> pad_cw(const snapgpu_ctx* c) {
+  std::vector<double> out;
+  size_t src = 0;
+  for (const Tuple& tp : c->maps.tuples)
+    for (int a2 = 0; a2 <= tp.j2; ++a2) {
+      for (int ma = 0; ma < cw_row(tp.j); ++ma) out.push_back(ma <= tp.j ? c->yplan.cw[src + ma] : 0.0);
+      src += tp.j + 1;
+    }
   return out;
 }
 
 void build_ycoop(snapgpu_ctx* c) {
   c->ycplan = ycoop_pair_plan(c->maps, kYGroupWarps);
+  c->yunit_rec = pack_units(c, c->ycplan);
+  const std::vector<double> cwp = pad_cw(c);
+  require(cwp.size() == (size_t)c_cwp_total(c->T), "compute_Y: C' table size mismatch");
+  c->d_cwp.alloc(cwp.size());
+  CK(cudaMemcpy(c->d_cwp.p, cwp.data(), cwp.size() * sizeof(double), cudaMemcpyHostToDevice));
   YTablesHost t;
-  t.cw = c->yplan.cw;
-  t.items = pack_units(c, c->ycplan);
   t.rw = c->ycplan.rw_begin;
   upload_ytables(c->device, c->T, t);
   upload_beta(c);
@@ -534,7 +559,7 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     up(c->d_weights, c->weights);
     c->yplan = y_plan(c->maps, cprime_table(c->maps, c->cg));
     up(c->d_expand, half_scatter_map(c->maps));
-    if (twojmax <= 8) {
+    if (twojmax <= SNAP_CWIN_MAXT) {
       // constant-window compute_Y: the windowed C' and the unit tables live
       // in the per-2J object's constant bank
       build_ycoop(c);
@@ -572,7 +597,8 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_weights.release();
   c->d_cw.release();
 
-  c->d_citw.release();
+  c->d_cwp.release();
+  c->d_yunits.release();
   c->d_qunits.release();
   c->d_qitw.release();
   c->d_qrw.release();

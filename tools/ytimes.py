@@ -2,6 +2,8 @@ import ctypes as C, sys
 import numpy as np
 sys.path.insert(0, '.')
 import paper_2011_12875_b200 as snap
+if len(sys.argv) > 1 and sys.argv[1].startswith("--lib="):  # the SNAP_Y_PROFILE build
+    snap.LIB_PATH = sys.argv.pop(1)[6:]
 p = snap.bcc_problem(10, 10, 10, twojmax=8)
 eng = snap.SnapEngine.for_problem(p); eng.set_problem(p); eng.enable_stage_timing(True)
 eng.run(); eng.synchronize()
@@ -26,3 +28,9 @@ for part in range(2):
 order = np.argsort(-d)
 print("slowest CTAs (block, sm, start us, dur us):", [(int(i), int(smid[i]), round(float(s[i]), 1), round(float(d[i]), 1)) for i in order[:12]])
 print("fastest:", [(int(i), int(smid[i]), round(float(s[i]), 1), round(float(d[i]), 1)) for i in order[-6:]])
+# TPC pairing: SMs 2k and 2k+1 share a TPC; is a CTA slower when its TPC partner is busy?
+busy = set(int(x) for x in smid)
+pd_ = [d[i] for i in range(len(d)) if (int(smid[i]) ^ 1) in busy]
+pa_ = [d[i] for i in range(len(d)) if (int(smid[i]) ^ 1) not in busy]
+print("TPC partner busy: n=%d median %.1f us; partner idle: n=%d median %.1f us" %
+      (len(pd_), np.median(pd_) if pd_ else 0, len(pa_), np.median(pa_) if pa_ else 0))
