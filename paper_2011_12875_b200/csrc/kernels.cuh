@@ -1303,8 +1303,20 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   unsigned long long g_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 #endif
-  for (int e = threadIdx.x; e < c_cwp_total(T) / 2; e += blockDim.x)
-    reinterpret_cast<double2*>(sC)[e] = __ldg(reinterpret_cast<const double2*>(A.cw) + e);
+  {  // C' -> shared: every load of a thread issued before its stores
+    constexpr int NC2 = c_cwp_total(T) / 2, KC = (NC2 + kYWarps * 32 - 1) / (kYWarps * 32);
+    double2 cv[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      const int e = threadIdx.x + k * kYWarps * 32;
+      if (e < NC2) cv[k] = __ldg(reinterpret_cast<const double2*>(A.cw) + e);
+    }
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      const int e = threadIdx.x + k * kYWarps * 32;
+      if (e < NC2) reinterpret_cast<double2*>(sC)[e] = cv[k];
+    }
+  }
   const int tile = blockIdx.x;
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
   pdl_wait();  // V comes from compute_U
