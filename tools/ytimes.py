@@ -11,7 +11,8 @@ L = snap.library(); buf = (C.c_longlong * 2112)()
 L.snapgpu_debug_yprof(buf, 2112)
 eng.run(); eng.synchronize()
 L.snapgpu_debug_yprof(buf, 2112)
-a = np.array(buf[64:64 + 2 * 126], dtype=np.int64).reshape(-1, 2)
+nb = int(buf[61])  # CTAs of the launch
+a = np.array(buf[64:64 + 2 * nb], dtype=np.int64).reshape(-1, 2)
 smid = a[:, 1] & 255
 a[:, 1] = a[:, 0] + (a[:, 1] >> 8)
 t0 = a[:, 0].min()
@@ -21,10 +22,6 @@ print("end   us: min %.1f med %.1f max %.1f" % (e.min(), np.median(e), e.max()))
 print("dur   us: min %.1f med %.1f max %.1f" % ((e - s).min(), np.median(e - s), (e - s).max()))
 print("stage times", eng.stage_times())
 d = e - s
-nx = 63
-for part in range(2):
-    dd = d[part * nx:(part + 1) * nx]
-    print("part", part, "dur us min %.1f med %.1f max %.1f" % (dd.min(), np.median(dd), dd.max()))
 order = np.argsort(-d)
 print("slowest CTAs (block, sm, start us, dur us):", [(int(i), int(smid[i]), round(float(s[i]), 1), round(float(d[i]), 1)) for i in order[:12]])
 print("fastest:", [(int(i), int(smid[i]), round(float(s[i]), 1), round(float(d[i]), 1)) for i in order[-6:]])
