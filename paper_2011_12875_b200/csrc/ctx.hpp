@@ -150,6 +150,12 @@ struct snapgpu_ctx {
   bool graph_valid = false;
   cudaGraph_t csr_graph = nullptr;
   cudaGraphExec_t csr_gexec = nullptr;
+  // the force step after a list upload: the reverse-index build forked onto
+  // side_stream, joined only before the force gather (its one consumer)
+  cudaGraph_t fork_graph = nullptr;
+  cudaGraphExec_t fork_gexec = nullptr;
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // one-call positions step (snapgpu_run_positions): pinned staging + graph
   cudaGraph_t pos_graph = nullptr;
   cudaGraphExec_t pos_gexec = nullptr;

@@ -1767,6 +1767,7 @@ struct GatherArgs {
   double* forces;
   int chunk_rows, chunk_stride, nchunks;
   const double* etotal;  // this rank's total (nchunks > 1)
+  unsigned* flags_out;   // the validation flags copied here (one-call read-back slot)
 };
 
 // One thread per (atom, component).  Up to kGatherCap reverse slots and own
@@ -1784,6 +1785,7 @@ __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
     pdl_wait();                           // (etotal comes from compute_Y)
     A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
   }
+  if (t == 0) *A.flags_out = *(volatile const unsigned*)A.pr.err;  // final after compute_U
   if (a >= A.pr.natoms_total) return;
   double* fo = A.forces + (size_t)(a / A.chunk_rows) * A.chunk_stride +
                (size_t)(a % A.chunk_rows) * 3 + d;

@@ -19,6 +19,10 @@ void invalidate_graph(snapgpu_ctx* c) {
   c->gexec = nullptr;
   c->graph = nullptr;
   c->graph_valid = false;
+  if (c->fork_gexec) cudaGraphExecDestroy(c->fork_gexec);
+  if (c->fork_graph) cudaGraphDestroy(c->fork_graph);
+  c->fork_gexec = nullptr;
+  c->fork_graph = nullptr;
 }
 
 void invalidate_pos_graph(snapgpu_ctx* c) {
@@ -266,6 +270,7 @@ void launch_gather(snapgpu_ctx* c) {
   a.chunk_stride = c->chunk_stride();
   a.nchunks = c->nchunks;
   a.etotal = c->d_etotal.p;
+  a.flags_out = reinterpret_cast<unsigned*>(c->d_out.p + c->d_forces.n + c->d_eatom.n + 1);
   const int nthr = std::max(3 * c->natoms_total, c->nchunks);
   if (c->natoms_total > 0) {  // one thread per force component
     launch_pdl(k_gather_forces, dim3((nthr + 127) / 128), dim3(128), 0, c->stream, a);
@@ -332,7 +337,11 @@ void set_lists(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int st
     c->d_forces.release();
     c->d_eatom.release();
     c->d_etotal.release();
-    c->d_out.alloc(nf + ne + 1);
+    // [forces | eatom | etotal | validation flags]: the gather copies the
+    // flags into the last slot, so a one-call step reads everything back
+    // with one D2H
+    c->d_out.alloc(nf + ne + 2);
+    CK(cudaMemsetAsync(c->d_out.p, 0, (nf + ne + 2) * sizeof(double), c->stream));
     c->d_forces.view(c->d_out.p, nf);
     c->d_eatom.view(c->d_out.p + nf, ne);
     c->d_etotal.view(c->d_out.p + nf + ne, 1);
@@ -549,6 +558,9 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     c->hf = half_f(c->maps);
     c->ywgt = half_ywgt(c->maps);
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->stream = c->own_stream;
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     auto up = [](auto& buf, const auto& v) {
@@ -633,6 +645,9 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_rev.release();
   c->d_err.release();
   if (c->h_err) cudaFreeHost(c->h_err);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return SNAPGPU_OK;
@@ -755,14 +770,51 @@ int snapgpu_run(snapgpu_ctx* c) {
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_lists, "run: no neighbor lists");
-    ensure_csr(c);
     if (c->timing) {
+      ensure_csr(c);
       run_direct(c);
       CK(cudaEventSynchronize(c->ev[4]));
       for (int s = 0; s < 4; ++s) CK(cudaEventElapsedTime(&c->stage_ms[s], c->ev[s], c->ev[s + 1]));
+    } else if (c->csr_dirty && !c->sym_lists) {
+      // new lists: the reverse-index build runs beside U / Y / dE (it only
+      // feeds the force gather), one graph with a fork and a join
+      if (!c->fork_gexec) {
+        cudaStream_t user = c->stream;
+        c->stream = c->own_stream;
+        CK(cudaStreamSynchronize(user));
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          CK(cudaEventRecord(c->ev_fork, c->own_stream));
+          CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+          c->stream = c->side_stream;
+          launch_rev_build(c);
+          CK(cudaEventRecord(c->ev_join, c->side_stream));
+          c->stream = c->own_stream;
+          launch_U(c);
+          launch_Y(c);
+          launch_dE(c);
+          CK(cudaStreamWaitEvent(c->own_stream, c->ev_join, 0));
+          launch_gather(c);
+        } catch (...) {
+          c->stream = c->own_stream;
+          cudaGraph_t g;
+          cudaStreamEndCapture(c->stream, &g);
+          if (g) cudaGraphDestroy(g);
+          c->stream = user;
+          throw;
+        }
+        CK(cudaStreamEndCapture(c->stream, &c->fork_graph));
+        CK(cudaGraphInstantiate(&c->fork_gexec, c->fork_graph, 0));
+        c->stream = user;
+      }
+      CK(cudaGraphLaunch(c->fork_gexec, c->stream));
+      c->csr_dirty = false;
     } else {
       if (!c->graph_valid) {
-        invalidate_graph(c);
+        if (c->gexec) cudaGraphExecDestroy(c->gexec);
+        if (c->graph) cudaGraphDestroy(c->graph);
+        c->gexec = nullptr;
+        c->graph = nullptr;
         cudaStream_t user = c->stream;
         c->stream = c->own_stream;  // capture on our own (non-legacy) stream
         CK(cudaStreamSynchronize(user));
@@ -798,10 +850,12 @@ int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, 
   const int rr = snapgpu_run(c);
   if (rr != SNAPGPU_OK) return rr;
   return guarded(c, [&] {
-    CK(cudaMemcpyAsync(c->h_err, c->d_err.p, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                       c->stream));
-    // one D2H of [forces | eatom | etotal] into pinned staging, then host copies
-    const size_t nf = c->d_forces.n, ne = c->d_eatom.n, nout = nf + ne + 1;
+    // one D2H of [forces | eatom | etotal | flags] into pinned staging, then
+    // host copies
+    const size_t nf = c->d_forces.n, ne = c->d_eatom.n, nout = nf + ne + 2;
+    if (c->natoms_total <= 0)  // no gather launched: flags straight into their slot
+      CK(cudaMemcpyAsync(c->d_out.p + nf + ne + 1, c->d_err.p, sizeof(unsigned),
+                         cudaMemcpyDeviceToDevice, c->stream));
     if (c->h_out_n < nout) {
       if (c->h_out) cudaFreeHost(c->h_out);
       c->h_out = nullptr;
@@ -818,8 +872,10 @@ int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, 
     if (forces && !c->ext_forces) std::memcpy(forces, c->h_out, sizeof(double) * force_doubles(c));
     if (eatom && c->nlocal > 0) std::memcpy(eatom, c->h_out + nf, sizeof(double) * c->nlocal);
     if (etotal) *etotal = c->h_out[nf + ne];
-    if (*c->h_err) {
-      const unsigned f = *c->h_err;
+    unsigned flags;
+    std::memcpy(&flags, c->h_out + nf + ne + 1, sizeof(unsigned));
+    if (flags) {
+      const unsigned f = flags;
       CK(cudaMemsetAsync(c->d_err.p, 0, sizeof(unsigned), c->stream));
       CK(cudaStreamSynchronize(c->stream));
       c->have_lists = c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
@@ -977,7 +1033,7 @@ int snapgpu_run_positions(snapgpu_ctx* c, int natoms, const double* pos, const d
     bool overflow = false;
     const int rc = guarded(c, [&] {
       require(natoms > 0, "run_positions: no atoms");
-      const size_t nf = c->d_forces.n, ne = c->d_eatom.n, nout = nf + ne + 1;
+      const size_t nf = c->d_forces.n, ne = c->d_eatom.n, nout = nf + ne + 2;
       if (c->h_out_n < nout) {
         if (c->h_out) cudaFreeHost(c->h_out);
         c->h_out = nullptr;
@@ -1015,8 +1071,6 @@ int snapgpu_run_positions(snapgpu_ctx* c, int natoms, const double* pos, const d
           run_direct(c);
           CK(cudaMemcpyAsync(c->h_out, c->d_out.p, nout * sizeof(double), cudaMemcpyDeviceToHost,
                              c->stream));
-          CK(cudaMemcpyAsync(c->h_err, c->d_err.p, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                             c->stream));
         } catch (...) {
           cudaGraph_t g;
           cudaStreamEndCapture(c->stream, &g);
@@ -1031,8 +1085,10 @@ int snapgpu_run_positions(snapgpu_ctx* c, int natoms, const double* pos, const d
       CK(cudaGraphLaunch(c->pos_gexec, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       c->have_U = c->have_Y = c->have_dE = c->have_forces = true;
-      if (*c->h_err) {
-        const unsigned f = *c->h_err;
+      unsigned flags;
+      std::memcpy(&flags, c->h_out + nf + ne + 1, sizeof(unsigned));
+      if (flags) {
+        const unsigned f = flags;
         CK(cudaMemsetAsync(c->d_err.p, 0, sizeof(unsigned), c->stream));
         CK(cudaStreamSynchronize(c->stream));
         c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
