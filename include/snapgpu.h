@@ -115,7 +115,12 @@ int snapgpu_synchronize(snapgpu_ctx* ctx);
  * atoms' lists (set_neighbors_partition semantics; atom_lo = 0 and nlocal =
  * natoms_total for a single GPU), run, and copy forces (natoms_total x 3),
  * eatom (nlocal) and etotal back (any output may be NULL); one stream
- * synchronization.  Equivalent to run_pipeline (pipeline.hpp:206-303). */
+ * synchronization.  Equivalent to run_pipeline (pipeline.hpp:206-303).
+ * When numneigh / nbr / disp are page-locked host memory (cudaHostAlloc,
+ * cudaHostRegister; mapped under UVA) and 2J <= 8, no copy is issued:
+ * compute_U reads them over PCIe while it computes and leaves the device
+ * copies for the later stages; pageable arrays are uploaded first.  The
+ * reverse-neighbor index is rebuilt beside Y / dE in either case. */
 int snapgpu_run_host(snapgpu_ctx* ctx, int natoms_total, int atom_lo, int nlocal,
                      int stride, const int* numneigh, const int* nbr,
                      const double* disp, const int* types, double* forces,

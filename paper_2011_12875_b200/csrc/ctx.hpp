@@ -139,6 +139,11 @@ struct snapgpu_ctx {
   // when nchunks > 1), into the caller's device buffer when ext_forces is set
   int nchunks = 1;
   double* ext_forces = nullptr;
+  // one-call step from pinned host lists: mapped host sources compute_U pulls
+  // the lists from (UArgs::src_*); set only for the duration of that launch
+  const int* zc_numneigh = nullptr;
+  const int* zc_nbr = nullptr;
+  const double* zc_disp = nullptr;
   int chunk_rows() const {
     return nchunks > 1 ? (natoms_total + nchunks - 1) / nchunks : (natoms_total > 0 ? natoms_total : 1);
   }

@@ -230,6 +230,13 @@ struct UArgs {
   GeoParams gp;
   double* V;  // [tile][2][NH][32]
   L2Prefetch pf;
+  // one-call step from pinned host lists (zero-copy): compute_U reads the
+  // lists straight from these mapped host arrays over PCIe, overlapping the
+  // transfer with its own work, and writes the device copies (pr.numneigh /
+  // nbr / disp) that the later stages read.  Null: the lists are on the device.
+  const int* src_numneigh;
+  const int* src_nbr;
+  const double* src_disp;
 };
 
 __device__ __forceinline__ void l2_prefetch(const L2Prefetch& P) {
@@ -495,19 +502,45 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
   double* geo = smem + (size_t)w * C::APW * S * 5;  // [atom][pair][ar ai br bi sfac]
 
   // ---- prepass: validation + geometry of the warp's pairs ----
+  // With pinned host lists (A.src_*) every slot, padding included, is read
+  // over PCIe here and stored to the device copies.  (Measured: a separate
+  // coalesced or 16-byte copy loop ahead of the prepass pulls no faster --
+  // GPU-initiated PCIe reads run at ~27-30 GB/s either way -- and exposes
+  // the transfer instead of interleaving it with the geometry.)
+  const bool pull = A.src_disp != nullptr;
   for (int idx = lane; idx < C::APW * S; idx += 32) {
     const int a = idx / S, k = idx - a * S;
     const int i = i0 + a;
     if (i >= A.pr.nlocal) continue;
-    int nn = A.pr.numneigh[i];
+    const size_t pk = (size_t)i * S + k;
+    int nn, j;
+    double d[3];
+    if (pull) {
+      nn = A.src_numneigh[i];
+      j = A.src_nbr[pk];
+      d[0] = A.src_disp[pk * 3 + 0];
+      d[1] = A.src_disp[pk * 3 + 1];
+      d[2] = A.src_disp[pk * 3 + 2];
+      if (k == 0) const_cast<int*>(A.pr.numneigh)[i] = nn;
+      const_cast<int*>(A.pr.nbr)[pk] = j;
+      double* dd = const_cast<double*>(A.pr.disp) + pk * 3;
+      dd[0] = d[0];
+      dd[1] = d[1];
+      dd[2] = d[2];
+    } else {
+      nn = A.pr.numneigh[i];
+    }
     if (nn < 0 || nn > S) {
       if (k == 0) atomicOr(A.pr.err, kErrCount);
       continue;
     }
     if (k >= nn) continue;
-    const size_t pk = (size_t)i * S + k;
-    const double* d = A.pr.disp + pk * 3;
-    const int j = A.pr.nbr[pk];
+    if (!pull) {
+      j = A.pr.nbr[pk];
+      d[0] = A.pr.disp[pk * 3 + 0];
+      d[1] = A.pr.disp[pk * 3 + 1];
+      d[2] = A.pr.disp[pk * 3 + 2];
+    }
     const double rsq = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
     unsigned bad = 0u;
     if (j < 0 || j >= A.pr.natoms_total) bad |= kErrIndex;
@@ -537,7 +570,7 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
   const int i = i0 + a;
   int nn = 0;
   if (i < A.pr.nlocal) {
-    nn = A.pr.numneigh[i];
+    nn = pull ? __ldcg(A.pr.numneigh + i) : A.pr.numneigh[i];  // (written by this warp)
     if (nn < 0 || nn > S) nn = 0;
   }
   int passes = (nn + C::SL * PP - 1) / (C::SL * PP);

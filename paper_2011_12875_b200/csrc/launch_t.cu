@@ -47,6 +47,9 @@ static void launch_U2(snapgpu_ctx* c) {
   a.gp = c->gp;
   a.V = c->d_V.p;
   a.pf = y_prefetch<T>(c);
+  a.src_numneigh = c->zc_numneigh;
+  a.src_nbr = c->zc_nbr;
+  a.src_disp = c->zc_disp;
   const size_t smem = sizeof(double) * (size_t)C2::WARPS * C2::APW * c->stride * 5;
   CK(cudaFuncSetAttribute(k_compute_U2<T, SL, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::max<size_t>(smem, 48 * 1024)));
@@ -72,6 +75,8 @@ void launch_U_t(snapgpu_ctx* c) {
     a.gp = c->gp;
     a.V = c->d_V.p;
     a.pf = L2Prefetch{};
+    a.src_numneigh = a.src_nbr = nullptr;  // (the one-call pull is T <= 8 only)
+    a.src_disp = nullptr;
     const size_t smem = sizeof(double) * ((size_t)C::WARPS * c->stride * 5 +
                                           (C::REGACC ? 0 : (size_t)C::WARPS * 2 * C::NACC * 32));
     CK(cudaFuncSetAttribute(k_compute_U<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -473,6 +473,49 @@ void record(snapgpu_ctx* c, int k) {
   if (c->timing) CK(cudaEventRecord(c->ev[k], c->stream));
 }
 
+// Device address of a mapped (pinned) host array, or null for pageable memory.
+const void* mapped_ptr(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (at.type == cudaMemoryTypeHost) ? at.devicePointer : nullptr;
+}
+
+// The one-call step from pinned host lists: compute_U pulls the lists over
+// PCIe while it computes (UArgs::src_*) and leaves the device copies; the
+// reverse-index build forks onto side_stream after it and joins before the
+// force gather.  Direct launches (the sources change every call).
+void run_pull(snapgpu_ctx* c, const int* nn, const int* nb, const double* dp) {
+  cudaStream_t main = c->stream;
+  c->zc_numneigh = nn;
+  c->zc_nbr = nb;
+  c->zc_disp = dp;
+  try {
+    launch_U(c);
+    c->zc_numneigh = c->zc_nbr = nullptr;
+    c->zc_disp = nullptr;
+    CK(cudaEventRecord(c->ev_fork, main));
+    CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+    c->stream = c->side_stream;
+    launch_rev_build(c);
+    CK(cudaEventRecord(c->ev_join, c->side_stream));
+    c->stream = main;
+    launch_Y(c);
+    launch_dE(c);
+    CK(cudaStreamWaitEvent(main, c->ev_join, 0));
+    launch_gather(c);
+  } catch (...) {
+    c->stream = main;
+    c->zc_numneigh = c->zc_nbr = nullptr;
+    c->zc_disp = nullptr;
+    throw;
+  }
+  c->csr_dirty = false;
+}
+
 void run_direct(snapgpu_ctx* c) {
   record(c, 0);
   launch_U(c);
@@ -843,12 +886,31 @@ int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, 
                      const int* numneigh, const int* nbr, const double* disp,
                      const int* types, double* forces, double* eatom, double* etotal) {
   if (!c) return SNAPGPU_EINVAL;
+  bool pulled = false;
   const int rc = guarded(c, [&] {
-    set_lists(c, natoms_total, atom_lo, nlocal, stride, numneigh, nbr, disp, types, false);
+    // pinned (mapped) host lists: no upload, compute_U pulls them itself
+    const void* zn = nullptr;
+    const void* zb = nullptr;
+    const void* zd = nullptr;
+    if (c->T <= 8 && nlocal > 0 && stride > 0 && !c->timing) {  // k_compute_U2
+      zn = mapped_ptr(numneigh);
+      zb = zn ? mapped_ptr(nbr) : nullptr;
+      zd = zb ? mapped_ptr(disp) : nullptr;
+    }
+    pulled = zd != nullptr;
+    set_lists(c, natoms_total, atom_lo, nlocal, stride, numneigh, nbr, disp, types, false,
+              !pulled);
+    if (pulled) {
+      run_pull(c, static_cast<const int*>(zn), static_cast<const int*>(zb),
+               static_cast<const double*>(zd));
+      c->have_U = c->have_Y = c->have_dE = c->have_forces = true;
+    }
   });
   if (rc != SNAPGPU_OK) return rc;
-  const int rr = snapgpu_run(c);
-  if (rr != SNAPGPU_OK) return rr;
+  if (!pulled) {
+    const int rr = snapgpu_run(c);
+    if (rr != SNAPGPU_OK) return rr;
+  }
   return guarded(c, [&] {
     // one D2H of [forces | eatom | etotal | flags] into pinned staging, then
     // host copies

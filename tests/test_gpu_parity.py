@@ -175,8 +175,46 @@ def test_errors_map_to_reference_exceptions(snap):
     eng.close()
 
 
+_PINNED_KEEP = []
+
+
+def _pinned(a):
+    """A page-locked (hence device-mapped) copy of `a` as a numpy array."""
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    _PINNED_KEEP.append(t)
+    return t.numpy()
+
+
+@pytest.mark.parametrize("T", [2, 5, 8, 10])
+def test_one_call_pinned_lists_pull(snap, port, T):
+    """snapgpu_run_host with pinned host lists: compute_U pulls them over PCIe
+    (2J <= 8; 2J > 8 uploads them) -- bitwise the result of the pageable-list
+    upload path, and within the parity bar of the oracle, on a ragged typed
+    cluster and on BCC lattices; the device copies it leaves serve a
+    following graph run."""
+    for p in (port.make_cluster(12, T, 91 + T), snap.bcc_problem(4, 4, 4, twojmax=T)):
+        p = snap.Problem.from_any(p)
+        ty = p.types
+        with snap.SnapEngine.for_problem(p) as eng:
+            f0, e0, t0 = eng.step(p.numneigh, p.nbr, p.disp, ty)
+            args = [_pinned(x) for x in (p.numneigh, p.nbr, p.disp)]
+            for _ in range(2):
+                f1, e1, t1 = eng.step(*args, ty)
+                assert np.array_equal(f1, f0) and np.array_equal(e1, e0) and t1 == t0
+            eng.run()  # graph run on the lists the pull left on the device
+            assert np.array_equal(eng.forces(), f0)
+            nn, nbr, disp = eng.neighbors()
+            assert np.array_equal(nn, p.numneigh) and np.array_equal(disp, p.disp)
+        ref = port.run(p, want=("forces", "etotal"))
+        assert np.abs(f1 - ref["forces"]).max() <= 1e-10 * np.abs(ref["forces"]).max()
+        assert abs(t1 - ref["etotal"]) <= 1e-12 * abs(ref["etotal"])
+
+
+@pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("case", ["cut", "self", "index", "zero", "count", "type"])
-def test_one_call_step_validates_on_device(snap, case):
+def test_one_call_step_validates_on_device(snap, case, pinned):
     """snapgpu_run_host defers Problem::validate (snap_core.hpp:89-118) to the
     U kernel: every violation still raises InvalidArgument with the host
     message, nothing is scattered, and the next valid step is exact."""
@@ -198,6 +236,8 @@ def test_one_call_step_validates_on_device(snap, case):
         nn[7] = nbr.shape[1] + 1
     else:
         types[8] = 3
+    if pinned:  # the compute_U pull path
+        nn, nbr, disp = (_pinned(x) for x in (nn, nbr, disp))
     with snap.SnapEngine.for_problem(p) as eng:
         with pytest.raises(snap.InvalidArgument, match=match):
             eng.step(nn, nbr, disp, types)
