@@ -144,6 +144,12 @@ struct snapgpu_ctx {
   const int* zc_numneigh = nullptr;
   const int* zc_nbr = nullptr;
   const double* zc_disp = nullptr;
+  // ... and its mapped host outputs, written by the kernels beside the
+  // device copies (EnergyOut / GatherArgs second sinks); null otherwise
+  double* sink_forces = nullptr;
+  double* sink_eatom = nullptr;
+  double* sink_etotal = nullptr;
+  unsigned* sink_flags = nullptr;
   int chunk_rows() const {
     return nchunks > 1 ? (natoms_total + nchunks - 1) / nchunks : (natoms_total > 0 ? natoms_total : 1);
   }
@@ -221,6 +227,8 @@ inline EnergyOut energy_out(snapgpu_ctx* c) {
   E.ticket = c->d_tickets.p;
   E.tile_ticket = c->d_tickets.p + 1;
   E.etotal = c->d_etotal.p;
+  E.eatom_host = c->sink_eatom;
+  E.etotal_host = c->sink_etotal;
   return E;
 }
 

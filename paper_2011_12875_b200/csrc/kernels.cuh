@@ -742,6 +742,10 @@ struct EnergyOut {
   unsigned* tile_ticket;  // [ntiles], zero at launch; reset by each tile's last CTA
   unsigned* ticket;       // zero at launch; reset by the last tile
   double* etotal;
+  // optional second sinks: the caller's mapped (pinned) host arrays of the
+  // one-call step, written beside the device copies (no read-back copy)
+  double* eatom_host;
+  double* etotal_host;
 };
 
 template <int APT>
@@ -761,7 +765,10 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
   double e = 0.0;
   if (lane < APT)
     for (unsigned q = 0; q < parts; ++q) e += __ldcg(E.epart + ((size_t)q * ntiles + tile) * APT + lane);
-  if (valid) E.eatom[atom] = e;
+  if (valid) {
+    E.eatom[atom] = e;
+    if (E.eatom_host) E.eatom_host[atom] = e;
+  }
   double s = valid ? e : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -780,6 +787,7 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) {
     *E.etotal = acc;
+    if (E.etotal_host) *E.etotal_host = acc;
     *E.ticket = 0u;
   }
 }
@@ -1801,6 +1809,9 @@ struct GatherArgs {
   int chunk_rows, chunk_stride, nchunks;
   const double* etotal;  // this rank's total (nchunks > 1)
   unsigned* flags_out;   // the validation flags copied here (one-call read-back slot)
+  // optional second sinks (mapped host memory of the one-call step)
+  double* forces_host;   // [natoms][3] (single chunk only)
+  unsigned* flags_host;
 };
 
 // One thread per (atom, component).  Up to kGatherCap reverse slots and own
@@ -1818,12 +1829,17 @@ __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
     pdl_wait();                           // (etotal comes from compute_Y)
     A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
   }
-  if (t == 0) *A.flags_out = *(volatile const unsigned*)A.pr.err;  // final after compute_U
+  if (t == 0) {  // final after compute_U
+    const unsigned fl = *(volatile const unsigned*)A.pr.err;
+    *A.flags_out = fl;
+    if (A.flags_host) *A.flags_host = fl;
+  }
   if (a >= A.pr.natoms_total) return;
   double* fo = A.forces + (size_t)(a / A.chunk_rows) * A.chunk_stride +
                (size_t)(a % A.chunk_rows) * 3 + d;
   if (pipeline_failed(A.pr)) {
     *fo = 0.0;
+    if (A.forces_host) A.forces_host[t] = 0.0;
     return;
   }
   const int S = A.pr.stride;
@@ -1876,6 +1892,7 @@ __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
     for (; s < e; ++s) f -= A.dedr[(size_t)A.rev[s] * 3 + d];
   }
   *fo = f;
+  if (A.forces_host) A.forces_host[t] = f;  // single chunk: t = 3 a + d
 }
 
 // ===========================================================================

@@ -200,9 +200,13 @@ def test_one_call_pinned_lists_pull(snap, port, T):
         with snap.SnapEngine.for_problem(p) as eng:
             f0, e0, t0 = eng.step(p.numneigh, p.nbr, p.disp, ty)
             args = [_pinned(x) for x in (p.numneigh, p.nbr, p.disp)]
-            for _ in range(2):
-                f1, e1, t1 = eng.step(*args, ty)
+            outs = [_pinned(np.full(x.shape, np.nan)) for x in (f0, e0, np.zeros(1))]
+            for it in range(3):  # pageable outputs (read back), then pinned (written in place)
+                o = {} if it == 0 else dict(zip(("forces", "eatom", "etotal"), outs))
+                f1, e1, t1 = eng.step(*args, ty, **o)
                 assert np.array_equal(f1, f0) and np.array_equal(e1, e0) and t1 == t0
+                if it:
+                    assert f1 is outs[0] and e1 is outs[1]
             eng.run()  # graph run on the lists the pull left on the device
             assert np.array_equal(eng.forces(), f0)
             nn, nbr, disp = eng.neighbors()
@@ -238,10 +242,14 @@ def test_one_call_step_validates_on_device(snap, case, pinned):
         types[8] = 3
     if pinned:  # the compute_U pull path
         nn, nbr, disp = (_pinned(x) for x in (nn, nbr, disp))
+    o = {}
+    if pinned:  # pinned outputs too: written in place by the kernels
+        o = dict(zip(("forces", "eatom", "etotal"),
+                     (_pinned(np.zeros(x)) for x in ((p.natoms, 3), p.natoms, 1))))
     with snap.SnapEngine.for_problem(p) as eng:
         with pytest.raises(snap.InvalidArgument, match=match):
-            eng.step(nn, nbr, disp, types)
-        f, e, t = eng.step(p.numneigh, p.nbr, p.disp)
+            eng.step(nn, nbr, disp, types, **o)
+        f, e, t = eng.step(p.numneigh, p.nbr, p.disp, **o)
         # deterministic force gather and energy reductions: bitwise equal
         assert np.array_equal(f, ref.forces)
         assert np.array_equal(e, ref.eatom)
