@@ -2089,9 +2089,31 @@ __global__ void __launch_bounds__(kNLWarps * 32) k_nl_lists_warp(const NLArgs A,
   }
   auto scan = [&](auto&& f) {
     if (A.cells) {
-      for (int s = s0; s < s1; ++s) {
-        const int k = A.members[s];
-        if (k != i && inside(k)) f(k);
+      // batches of 4 candidates: member ids, then their positions, as
+      // independent loads (one latency per batch instead of two per atom)
+      constexpr int B = 4;
+      for (int s = s0; s < s1; s += B) {
+        int k[B];
+        double px[B], py[B], pz[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) k[u] = (s + u < s1) ? A.members[s + u] : -1;
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int kk = k[u] < 0 ? i : k[u];
+          px[u] = A.w[kk * 3];
+          py[u] = A.w[kk * 3 + 1];
+          pz[u] = A.w[kk * 3 + 2];
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          if (k[u] < 0 || k[u] == i) continue;
+          const double dx = nl_min_image(__dsub_rn(px[u], xi), A.box[0]);
+          const double dy = nl_min_image(__dsub_rn(py[u], yi), A.box[1]);
+          const double dz = nl_min_image(__dsub_rn(pz[u], zi), A.box[2]);
+          const double r2 =
+              __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+          if (r2 < A.rc2) f(k[u]);
+        }
       }
     } else {
       for (int k = lane; k < A.n; k += 32)
