@@ -25,9 +25,14 @@ value    : whole-job Katom-steps/s (harness.hpp:443-447 grind definition),
            device-timed with CUDA events per step on the engine stream, L2
            flushed (256 MiB write) before every timed step, max over ranks.
 e2e      : the same metric through the public one-call API with HOST
-           buffers: every step uploads that step's neighbor lists from pinned
-           memory (deferred Problem::validate on the device, reverse-index
-           rebuild) and reads forces and energies back (wall clock, synced).
+           buffers (wall clock, synced every call): every step moves that
+           step's neighbor lists from pinned host memory to the GPU --
+           compute_U reads them over PCIe while it computes and leaves the
+           device copies (zero-copy; h2d_bytes_per_step counts them) --,
+           validates them on the device, rebuilds the reverse index beside
+           Y / dE, and lands forces and energies in the caller's pinned
+           arrays (d2h_bytes_per_step).  e2e.positions: positions in, lists
+           rebuilt on the device inside the step graph.
 roofline : FP64 SIMT (the CG contraction is sparse FP64; no tensor-core path):
            algorithmic FLOPs of the dominant kernel (paper_2011_12875_b200.
            flops, reference loop nests, mul and add counted separately) / its
@@ -420,7 +425,8 @@ def run_ours(args):
         e2e = {"value": N * args.steps / t_e2e / 1000.0, "unit": "Katom-steps/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": t_e2e * 1e3 / args.steps,
-               "path": "snapgpu_run_host: neighbor lists in, forces/energies out"}
+               "path": "snapgpu_run_host: pinned neighbor lists in (read over PCIe by "
+                       "compute_U), forces/energies out into pinned arrays"}
         if n_gpus == 1:
             # the MD-loop call: positions in (neighbor lists rebuilt on the
             # device every step inside the same graph), forces/energies out
