@@ -1527,19 +1527,36 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
   const int p = (blockIdx.x * C::WARPS + w) * C::PPW + q;
   const int S = A.pr.stride;
   const int i = p / S, k = p - i * S;
-  const bool valid = (p < A.nslots) && (k < A.pr.numneigh[min(i, A.pr.nlocal - 1)]);
+  // the count, the displacement and the neighbor index as independent loads
+  // (the slot arrays are padded: every p < nslots is in bounds)
+  const bool in = p < A.nslots;
+  const int nn = A.pr.numneigh[min(i, A.pr.nlocal - 1)];
   double x = 1.0, y = 0.0, z = 0.0, wt = 0.0;
-  if (valid) {
+  int jn = 0;
+  if (in) {
     const double* d = A.pr.disp + (size_t)p * 3;
     x = d[0];
     y = d[1];
     z = d[2];
-    wt = neighbor_weight(A.pr, A.pr.nbr[p]);
+    jn = A.pr.nbr[p];
   }
-  PairGeo g;
-  pair_geometry<true>(x, y, z, wt, A.gp, g);
+  const bool valid = in && k < nn;
+  if (valid) {
+    wt = neighbor_weight(A.pr, jn);
+  } else {
+    x = 1.0;
+    y = z = 0.0;
+  }
   const int ia = valid ? i : 0;
   const double2* Y2 = reinterpret_cast<const double2*>(A.Y) + (size_t)ia * C::NH;
+  constexpr int NLINE = (C::NH * 16 + 127) / 128;  // 128-byte lines of one atom's Y'
+  // warm L2 with the atom's Y' (HBM-resident at large N) while the forward
+  // sweep runs; L2 is the coherence point, so this is safe before pdl_wait
+#pragma unroll
+  for (int m = r; m < NLINE; m += C::G)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(Y2) + 128 * m));
+  PairGeo g;
+  pair_geometry<true>(x, y, z, wt, A.gp, g);
   double* buf = sbuf + (size_t)w * C::NIN * 2 * 32 + lane;  // [elem][re|im][lane]
   const int s0 = (2 * r > 1) ? 2 * r : 1;                    // first level whose input row r stores
   auto in_off = [&](int t) { return (t * (t - 1) - s0 * (s0 - 1)) / 2; };
@@ -1594,7 +1611,6 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
   {  // the atom's Y' (NH x 16 B) into L1 at once: the row lanes of the pair
      // split its 128-byte lines, so the sweep's level-by-level loads hit L1
      // (262k atoms: dE 3.80 -> 3.68 ms)
-    constexpr int NLINE = (C::NH * 16 + 127) / 128;
     const char* yb = reinterpret_cast<const char*>(Y2);
 #pragma unroll
     for (int m = r; m < NLINE; m += C::G)
