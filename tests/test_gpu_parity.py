@@ -216,6 +216,30 @@ def test_one_call_pinned_lists_pull(snap, port, T):
         assert abs(t1 - ref["etotal"]) <= 1e-12 * abs(ref["etotal"])
 
 
+def test_one_call_partition_slab_pinned(snap):
+    """snapgpu_run_host on a rank's slab (atom_lo > 0, nlocal < natoms_total:
+    set_neighbors_partition semantics) with pinned lists: the partial forces
+    equal the pageable-upload path bitwise, and the slabs' partial forces sum
+    to the single-GPU forces (to round-off: the sum order differs)."""
+    p = snap.bcc_problem(6, 6, 6, twojmax=8)
+    ref = snap.run_pipeline(p)
+    n = p.natoms
+    tot = np.zeros((n, 3))
+    etot = 0.0
+    for lo, hi in ((0, n // 3), (n // 3, n)):
+        sl = [np.ascontiguousarray(x[lo:hi]) for x in (p.numneigh, p.nbr, p.disp)]
+        with snap.SnapEngine.for_problem(p) as eng:
+            f0, e0, t0 = eng.step(*sl, natoms_total=n, atom_lo=lo)
+            f0 = f0.copy()
+            f1, e1, t1 = eng.step(*[_pinned(x) for x in sl], natoms_total=n, atom_lo=lo)
+        assert np.array_equal(f1, f0) and np.array_equal(e1, e0) and t1 == t0
+        assert np.abs(e1 - ref.eatom[lo:hi]).max() <= 1e-12 * np.abs(ref.eatom).max()
+        tot += f1
+        etot += t1
+    assert normerr(tot, ref.forces) <= 1e-12
+    assert abs(etot - ref.etotal) <= 1e-12 * abs(ref.etotal)
+
+
 @pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("case", ["cut", "self", "index", "zero", "count", "type"])
 def test_one_call_step_validates_on_device(snap, case, pinned):
