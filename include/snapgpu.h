@@ -201,8 +201,15 @@ int snapgpu_enable_stage_timing(snapgpu_ctx* ctx, int on);
 int snapgpu_stage_times(snapgpu_ctx* ctx, float* out4);
 
 /* compute_Y launch knob (benchmark sweeps, 2J <= 8): CTAs per 32-atom tile
- * splitting its target rows, in [1, 8]; 0 = automatic (fill the SMs). */
+ * splitting its target rows, in [1, 8]; 0 = automatic (fill the SMs: the
+ * first tiles get one part more). */
 int snapgpu_tune(snapgpu_ctx* ctx, int y_parts);
+/* compute_Y -> compute_fused_dE hand-off (2J <= 8): on (default), dE starts
+ * per 32-atom tile as soon as compute_Y has written that tile's Y' (its CTAs
+ * take the SMs of finished tiles); off, dE waits for the whole compute_Y
+ * grid.  Results are bitwise identical.  Off by default when a tool is
+ * injected (ncu, compute-sanitizer), which may serialize the grids. */
+int snapgpu_set_overlap(snapgpu_ctx* ctx, int on);
 
 /* Force output layout for the atom-partitioned multi-GPU step
  * (the coupling is scatter_forces snap_core.hpp:889-898 and

@@ -100,6 +100,7 @@ def library() -> C.CDLL:
     L.snapgpu_enable_stage_timing.argtypes = [vp, ip]
     L.snapgpu_stage_times.argtypes = [vp, vp]
     L.snapgpu_tune.argtypes = [vp, ip]
+    L.snapgpu_set_overlap.argtypes = [vp, ip]
     L.snapgpu_set_force_layout.argtypes = [vp, ip, vp]
     L.snapgpu_counts.argtypes = [ip, vp]
     L.snapgpu_build_neighborlist.argtypes = [vp, ip, vp, dp, ip, vp, vp, vp]
@@ -371,6 +372,11 @@ class SnapEngine:
     def tune(self, y_parts=0):
         """compute_Y CTAs per 32-atom tile, 1..8 (0 = automatic)."""
         self._c(self._L.snapgpu_tune(self._h, int(y_parts)))
+
+    def set_overlap(self, on=True):
+        """compute_fused_dE starting per tile while compute_Y runs (2J <= 8;
+        default on, off under ncu / compute-sanitizer)."""
+        self._c(self._L.snapgpu_set_overlap(self._h, int(bool(on))))
 
     def set_force_layout(self, nchunks=1, ext_forces_ptr=None):
         """Chunked force output for the partitioned multi-GPU step

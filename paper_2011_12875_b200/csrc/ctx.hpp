@@ -102,8 +102,16 @@ struct snapgpu_ctx {
   snapgpu::host::DevBuf<int4> d_qunits;
   snapgpu::host::DevBuf<double> d_qitw;
   snapgpu::host::DevBuf<int> d_qrw, d_qrows;
-  int task_cap = 0;
-  int y_parts = 0, y_parts_used = 1;  // compute_Y CTAs per 32-atom tile (0 = automatic)
+  int y_parts = 0;        // compute_Y CTAs per 32-atom tile forced by snapgpu_tune (0 = automatic)
+  int y_parts_max = 1;    // the most parts any tile has in the current plan
+  int y_ctas = 0;         // compute_Y grid (2J <= 8): one CTA per (tile, part)
+  snapgpu::host::DevBuf<int4> d_ycta;    // per CTA {tile, part | parts << 8, row list, stride}
+  snapgpu::host::DevBuf<unsigned> d_ready;  // [ntiles] tile flags + [1] etotal flag (Y -> dE)
+  // compute_fused_dE starts per tile while compute_Y still runs (2J <= 8).
+  // Off when a tool is injected (ncu: CUDA_INJECTION64_PATH, compute-
+  // sanitizer: NV_SANITIZER_INJECTION_*): tools may serialize the grids, and
+  // a dE CTA waiting for a tile would then wait for a CTA that cannot run.
+  bool y_overlap = true;
 
   // problem shape
   int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
@@ -229,6 +237,9 @@ inline EnergyOut energy_out(snapgpu_ctx* c) {
   E.etotal = c->d_etotal.p;
   E.eatom_host = c->sink_eatom;
   E.etotal_host = c->sink_etotal;
+  E.pstride = c->y_parts_max;
+  E.ready = nullptr;  // set by the 2J <= 8 compute_Y launch
+  E.done = nullptr;
   return E;
 }
 

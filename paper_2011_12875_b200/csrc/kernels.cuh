@@ -737,7 +737,8 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
 // ---------------------------------------------------------------------------
 struct EnergyOut {
   double* eatom;          // [nlocal]
-  double* epart;          // [parts][ntiles][APT] per-CTA lane energies
+  double* epart;          // [ntiles][pstride][APT] per-CTA lane energies
+  int pstride;            // part slots per tile (the most parts any tile has)
   double* tile_sum;       // [ntiles]
   unsigned* tile_ticket;  // [ntiles], zero at launch; reset by each tile's last CTA
   unsigned* ticket;       // zero at launch; reset by the last tile
@@ -746,15 +747,30 @@ struct EnergyOut {
   // one-call step, written beside the device copies (no read-back copy)
   double* eatom_host;
   double* etotal_host;
+  // compute_Y -> compute_fused_dE hand-off per 32-atom tile (2J <= 8; null
+  // otherwise): ready[tile] = 1 once every part of the tile wrote its Y'
+  // rows, *done = 1 once etotal is final.  Reset by each tile's part 0 at
+  // its start (before the CTA lets the dependents launch).
+  unsigned* ready;
+  unsigned* done;
 };
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <int APT>
 __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_e, bool valid,
-                                                int atom) {
+                                                int atom, unsigned tile, unsigned part,
+                                                unsigned parts, unsigned ntiles) {
   // called by one full warp of the CTA; lanes >= APT carry no atom
   const int lane = threadIdx.x & 31;
-  const unsigned tile = blockIdx.x, ntiles = gridDim.x, parts = gridDim.y;
-  if (lane < APT) E.epart[((size_t)blockIdx.y * ntiles + tile) * APT + lane] = valid ? lane_e : 0.0;
+  if (lane < APT) E.epart[((size_t)tile * E.pstride + part) * APT + lane] = valid ? lane_e : 0.0;
   __threadfence();
   __syncwarp();
   unsigned t = 0;
@@ -764,7 +780,7 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
   __threadfence();  // this CTA saw every part of its tile
   double e = 0.0;
   if (lane < APT)
-    for (unsigned q = 0; q < parts; ++q) e += __ldcg(E.epart + ((size_t)q * ntiles + tile) * APT + lane);
+    for (unsigned q = 0; q < parts; ++q) e += __ldcg(E.epart + ((size_t)tile * E.pstride + q) * APT + lane);
   if (valid) {
     E.eatom[atom] = e;
     if (E.eatom_host) E.eatom_host[atom] = e;
@@ -776,6 +792,7 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
     E.tile_sum[tile] = s;
     E.tile_ticket[tile] = 0u;
     __threadfence();
+    if (E.ready) st_release(E.ready + tile, 1u);  // every part's Y' rows are out
     t = atomicAdd(E.ticket, 1u);
   }
   t = __shfl_sync(0xffffffffu, t, 0);
@@ -788,6 +805,10 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
   if (lane == 0) {
     *E.etotal = acc;
     if (E.etotal_host) *E.etotal_host = acc;
+    if (E.done) {
+      __threadfence();
+      st_release(E.done, 1u);
+    }
     *E.ticket = 0u;
   }
 }
@@ -1020,7 +1041,8 @@ __global__ void __launch_bounds__(kQWarps * 32, 1) k_compute_Y_quad(const YQArgs
     s += __shfl_xor_sync(0xffffffffu, s, 8);
     s += __shfl_xor_sync(0xffffffffu, s, 16);
     const int atom = atom0 + a;
-    energy_epilogue<8>(A.E, (2.0 / 3.0) * s, lane < 8 && atom < A.nlocal, atom);
+    energy_epilogue<8>(A.E, (2.0 / 3.0) * s, lane < 8 && atom < A.nlocal, atom, blockIdx.x,
+                       blockIdx.y, gridDim.y, gridDim.x);
   }
 }
 
@@ -1189,8 +1211,10 @@ struct YWArgs {
   const YUnit* units;   // unit records + W
   const double* cw;     // padded windowed C' (staged into shared memory)
   long long* prof;      // SNAP_Y_PROFILE builds: per-row cycle sums (else unused)
-  const int* tasks;
-  int task_cap;
+  const int* tasks;    // row lists (-1 terminated), per (part, warp group)
+  const int4* cta;     // per CTA: {tile, part | parts << 8, its first row list, list stride}
+  int ntiles;
+  int early;           // let compute_fused_dE launch once every CTA is resident (per-tile hand-off)
   int nlocal;
   EnergyOut E;
 };
@@ -1358,7 +1382,15 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
       if (e < NC2) reinterpret_cast<double2*>(sC)[e] = cv[k];
     }
   }
-  const int tile = blockIdx.x;
+  // This CTA's share: the tiles are split over a varying number of parts so
+  // that the CTAs fill the SMs exactly (snapgpu.cu plan_y).
+  const int4 ci = __ldg(A.cta + blockIdx.x);
+  const int tile = ci.x, part = ci.y & 0xff, parts = ci.y >> 8;
+  if (part == 0 && threadIdx.x == 0 && A.E.ready) {  // this step's hand-off starts empty
+    A.E.ready[tile] = 0u;
+    if (tile == 0) *A.E.done = 0u;
+    __threadfence();
+  }
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
   pdl_wait();  // V comes from compute_U
   for (int e = threadIdx.x; e < kXPad * 32; e += blockDim.x) {
@@ -1398,9 +1430,13 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     }
   }
   __syncthreads();
+  // every CTA of the grid is resident once all have passed here: let
+  // compute_fused_dE launch now; it waits per tile (E.ready), so its CTAs
+  // take the SMs of finished tiles while the other tiles still run
+  if (A.early) pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = w / kYGW, wg = w - g * kYGW;
-  const int* tasks = A.tasks + (size_t)(blockIdx.y * GR + g) * A.task_cap;
+  const int* tasks = A.tasks + ci.z + (size_t)g * ci.w;
   double* sredg = sred + (size_t)g * (kYGW - 1) * (T + 1) * 2 * 32;
   double* Yt = A.Y + (size_t)(tile * 32 + lane) * NH * 2;  // Y' atom-major, interleaved complex
   double e_acc = 0.0;
@@ -1436,21 +1472,23 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
     t_prev = t_now;
 #endif
   }
-  pdl_trigger();  // this CTA's rows are done: let compute_dE start launching
+  if (!A.early) pdl_trigger();  // this CTA's rows are done
   se[w][lane] = e_acc;
+  __threadfence();  // every warp's Y' rows visible device-wide before the tile's flag
   __syncthreads();
   if (w == 0) {
     double s = 0.0;
     for (int q = 0; q < nw; ++q) s += se[q][lane];
     const int atom = tile * 32 + lane;
-    energy_epilogue<32>(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom);
+    energy_epilogue<32>(A.E, (2.0 / 3.0) * s, atom < A.nlocal, atom, tile, part, parts,
+                        A.ntiles);
 #ifdef SNAP_Y_PROFILE
     if (lane == 0 && A.prof) {
       atomicAdd(reinterpret_cast<unsigned long long*>(A.prof) + 62,
                 (unsigned long long)(clock64() - t_start));
       unsigned long long g_end;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-      const int b = blockIdx.y * gridDim.x + blockIdx.x;
+      const int b = blockIdx.x;
       if (b < 1024) {  // [64 + 2b]: start, end (ns)
         reinterpret_cast<unsigned long long*>(A.prof)[64 + 2 * b] = g_start;
         unsigned smid;
@@ -1496,6 +1534,7 @@ struct DEArgs {
   const double* Y;  // Y' stored
   double* dedr;     // [nlocal*stride][3]
   int nslots;       // nlocal*stride
+  const unsigned* ready;  // compute_Y's per-tile flags (2J <= 8), else null: grid wait
 };
 
 template <int T>
@@ -1607,7 +1646,39 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
   }
   __syncwarp();
 
-  pdl_wait();  // Y' comes from compute_Y: everything above overlapped its tail
+  if (A.ready) {
+    // Y' of this warp's atoms: wait for their tiles only.  compute_Y lets
+    // this grid launch once all its CTAs are resident, so every tile finishes
+    // without this grid's resources (no deadlock).  One lane per warp polls
+    // with backoff (hundreds of CTAs may wait while compute_Y still runs;
+    // per-thread polling would load the L2 slice of the flags; per-CTA
+    // polling would hold every warp for the CTA's slowest forward sweep),
+    // bounded at 2 ms of globaltimer: should the grids ever
+    // not run concurrently (a time-sliced GPU), it falls back to waiting for
+    // compute_Y's whole grid, which is always correct.
+    int late = 0;
+    if (lane == 0) {
+      const int p0 = (blockIdx.x * C::WARPS + w) * C::PPW;
+      const int p1 = min(p0 + C::PPW, A.nslots) - 1;
+      const int t0 = (min(p0, A.nslots - 1) / S) >> 5, t1 = (min(p1 / S, A.pr.nlocal - 1)) >> 5;
+      unsigned long long g0, g1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+      for (int t = t0; t <= t1 && !late; ++t)
+        while (ld_acquire(A.ready + t) == 0u) {
+          __nanosleep(500);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+          if (g1 - g0 > 2000000ull) {
+            late = 1;
+            break;
+          }
+        }
+    }
+    late = __shfl_sync(0xffffffffu, late, 0);
+    __syncwarp();  // lane 0's acquire orders the warp's Y' loads after it
+    if (late) pdl_wait();
+  } else {
+    pdl_wait();  // Y' comes from compute_Y: everything above overlapped its tail
+  }
   {  // the atom's Y' (NH x 16 B) into L1 at once: the row lanes of the pair
      // split its 128-byte lines, so the sweep's level-by-level loads hit L1
      // (262k atoms: dE 3.80 -> 3.68 ms)
@@ -1833,6 +1904,7 @@ struct GatherArgs {
   double* forces;
   int chunk_rows, chunk_stride, nchunks;
   const double* etotal;  // this rank's total (nchunks > 1)
+  const unsigned* ydone; // compute_Y's "etotal final" flag (2J <= 8), else null
   unsigned* flags_out;   // the validation flags copied here (one-call read-back slot)
   // optional second sinks (mapped host memory of the one-call step)
   double* forces_host;   // [natoms][3] (single chunk only)
@@ -1852,7 +1924,9 @@ __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
   const int a = t / 3, d = t - 3 * (t / 3);
   if (A.nchunks > 1 && t < A.nchunks) {  // this rank's energy into every chunk's slot
     pdl_wait();                           // (etotal comes from compute_Y)
-    A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = *A.etotal;
+    if (A.ydone)  // compute_fused_dE no longer waits for compute_Y's end
+      while (ld_acquire(A.ydone) == 0u) __nanosleep(200);
+    A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = __ldcg(A.etotal);
   }
   if (t == 0) {  // final after compute_U
     const unsigned fl = *(volatile const unsigned*)A.pr.err;

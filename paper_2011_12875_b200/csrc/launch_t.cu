@@ -107,12 +107,16 @@ void launch_Y_t(snapgpu_ctx* c) {
   a.prof = g_yprof;
 #endif
   a.tasks = c->d_tasks.p;
-  a.task_cap = c->task_cap;
+  a.cta = c->d_ycta.p;
+  a.ntiles = c->ntiles;
+  a.early = c->y_overlap ? 1 : 0;
   a.nlocal = c->nlocal;
   a.E = energy_out(c);
+  a.E.ready = c->d_ready.p;  // the per-tile hand-off to compute_fused_dE
+  a.E.done = c->d_ready.p + c->ntiles;
   const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYRedSlots * (T + 1) * 2 * 32 +
                                         (size_t)c_cwp_total(T));
-  dim3 grid(c->ntiles, c->y_parts_used);
+  dim3 grid(c->y_ctas);
   CK(cudaFuncSetAttribute(k_compute_Y_cwin<T, kYGroups>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   launch_pdl(k_compute_Y_cwin<T, kYGroups>, grid, dim3(kYWarps * 32), smem, c->stream, a);
@@ -172,6 +176,8 @@ void launch_DE_t(snapgpu_ctx* c) {
   a.Y = c->d_Y.p;
   a.dedr = c->d_dedr.p;
   a.nslots = c->nlocal * c->stride;
+  // 2J <= 8: wait per tile on compute_Y's flags instead of for its whole grid
+  a.ready = (T <= SNAP_CWIN_MAXT && c->y_overlap) ? c->d_ready.p : nullptr;
   const int per_block = R::WARPS * R::PPW;
   const int blocks = (a.nslots + per_block - 1) / per_block;
   if (blocks > 0) {

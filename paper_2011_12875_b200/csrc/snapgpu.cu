@@ -83,24 +83,66 @@ void upload_ytables(int device, int T, const YTablesHost& t) {
 void build_ycoop(snapgpu_ctx* c);
 
 void plan_y(snapgpu_ctx* c) {
-  int parts = 1;
+  int pmax = 1;
+  const int ntiles = std::max(1, c->ntiles);
   if (c->T <= SNAP_CWIN_MAXT) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-    parts = c->y_parts;
-    // one CTA per SM: never exceed a single wave
-    if (parts <= 0) parts = std::max(1, std::min(kMaxYParts, nsm / std::max(1, c->ntiles)));
-    // one row list per (part, warp group)
-    std::vector<int> tasks =
-        y_row_schedule(c->maps, c->ycplan.row_cost, parts * kYGroups, &c->task_cap);
+    // Parts (CTAs) per 32-atom tile, each taking an LPT share of the tile's
+    // rows.  With fewer tiles than SMs the tiles get floor(nsm / ntiles)
+    // parts and the first nsm mod ntiles tiles one more, so the grid is
+    // exactly one CTA per SM: those tiles finish early and their SMs take
+    // the first compute_fused_dE CTAs (which wait per tile, E.ready) while
+    // the other tiles still run.  snapgpu_tune forces a uniform count.
+    std::vector<int> P(ntiles, 1);
+    if (c->y_parts > 0) {
+      std::fill(P.begin(), P.end(), c->y_parts);
+    } else if (c->ntiles < nsm) {
+      const int base = std::max(1, std::min(kMaxYParts, nsm / ntiles));
+      int extra = base < kMaxYParts ? std::min(ntiles, nsm - base * ntiles) : 0;
+      // an even number of base tiles, so every TPC of the long-running CTAs
+      // pairs the same (parts, part) row lists (see the CTA order below);
+      // an odd group is left to the short extra-part CTAs
+      if (extra > 0 && ((ntiles - extra) & 1)) --extra;
+      for (int t = 0; t < ntiles; ++t) P[t] = base + (t < extra ? 1 : 0);
+    }
+    // one row schedule per distinct part count: parts x kYGroups row lists
+    std::vector<int> tasks;
+    int off[kMaxYParts + 1] = {}, cap[kMaxYParts + 1] = {};
+    for (int q = 1; q <= kMaxYParts; ++q) {
+      if (std::find(P.begin(), P.end(), q) == P.end()) continue;
+      std::vector<int> sched = y_row_schedule(c->maps, c->ycplan.row_cost, q * kYGroups, &cap[q]);
+      off[q] = static_cast<int>(tasks.size());
+      tasks.insert(tasks.end(), sched.begin(), sched.end());
+      pmax = std::max(pmax, q);
+    }
+    // CTA order: by part count (the long-running fewer-part CTAs first), then
+    // part, then tile.  Consecutive CTAs land
+    // on the two SMs of a TPC, which share an instruction cache; CTAs of the
+    // same (parts, part) run the same row lists, hence the same code (tile-
+    // major order made TPC partners run different rows: 2000 atoms, every
+    // row ~1.5x slower).
+    std::vector<int4> cta;
+    for (int q = 1; q <= kMaxYParts; ++q)
+      for (int part = 0; part < q; ++part)
+        for (int t = 0; t < ntiles; ++t)
+          if (P[t] == q)
+            cta.push_back(make_int4(t, part | (q << 8), off[q] + part * kYGroups * cap[q], cap[q]));
+    c->y_ctas = static_cast<int>(cta.size());
     c->d_tasks.alloc(tasks.size());
     CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->d_ycta.alloc(cta.size());
+    CK(cudaMemcpy(c->d_ycta.p, cta.data(), cta.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    c->d_ready.alloc((size_t)ntiles + 1);
+    CK(cudaMemsetAsync(c->d_ready.p, 0, sizeof(unsigned) * ((size_t)ntiles + 1), c->stream));
+  } else if (c->y_parts > 0) {
+    pmax = c->y_parts;
   }
-  c->y_parts_used = parts;
+  c->y_parts_max = pmax;
   // energy epilogue: per-CTA lane energies, per-tile sums and tickets (the
   // 2J > 8 kernel has 4 tiles of 8 atoms per 32-atom V tile)
-  const size_t nt = (size_t)std::max(1, c->ntiles);
-  c->d_epart.alloc((size_t)parts * nt * 32);
+  const size_t nt = (size_t)ntiles;
+  c->d_epart.alloc((size_t)pmax * 4 * nt * 32);
   c->d_tile_sum.alloc(4 * nt);
   c->d_tickets.alloc(1 + 4 * nt);
   CK(cudaMemsetAsync(c->d_tickets.p, 0, sizeof(unsigned) * (1 + 4 * nt), c->stream));
@@ -270,6 +312,8 @@ void launch_gather(snapgpu_ctx* c) {
   a.chunk_stride = c->chunk_stride();
   a.nchunks = c->nchunks;
   a.etotal = c->d_etotal.p;
+  a.ydone = (c->T <= SNAP_CWIN_MAXT && c->y_overlap && c->d_ready.p)
+                ? c->d_ready.p + std::max(1, c->ntiles) : nullptr;
   a.flags_out = reinterpret_cast<unsigned*>(c->d_out.p + c->d_forces.n + c->d_eatom.n + 1);
   a.forces_host = c->sink_forces;
   a.flags_host = c->sink_flags;
@@ -584,6 +628,12 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     CK(cudaSetDevice(device));
     c = new snapgpu_ctx();
     c->device = device;
+    {  // tools that inject themselves (ncu: CUDA_INJECTION64_PATH;
+       // compute-sanitizer: NV_SANITIZER_INJECTION_*) may serialize grids
+      const char* inj = std::getenv("CUDA_INJECTION64_PATH");
+      const char* san = std::getenv("NV_SANITIZER_INJECTION_PORT_BASE");
+      c->y_overlap = !((inj && *inj) || (san && *san));
+    }
     c->T = twojmax;
     c->d_err.alloc(1);
     CK(cudaMemset(c->d_err.p, 0, sizeof(unsigned)));
@@ -665,6 +715,8 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_virial.release();
   c->d_expand.release();
   c->d_tasks.release();
+  c->d_ycta.release();
+  c->d_ready.release();
   c->d_numneigh.release();
   c->d_nbr.release();
   c->d_types.release();
@@ -1356,6 +1408,16 @@ int snapgpu_tune(snapgpu_ctx* c, int y_parts) {
     invalidate_graph(c);
     invalidate_pos_graph(c);
     if (c->have_lists) plan_y(c);
+  });
+}
+
+int snapgpu_set_overlap(snapgpu_ctx* c, int on) {
+  if (!c) return SNAPGPU_EINVAL;
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->stream));
+    c->y_overlap = on != 0;
+    invalidate_graph(c);
+    invalidate_pos_graph(c);
   });
 }
 

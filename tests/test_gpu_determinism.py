@@ -152,3 +152,31 @@ def test_one_call_positions_step(snap):
         pr.numneigh, pr.nbr, pr.disp = nn, nbr, disp
         r = snap.run_pipeline(pr)
         assert np.array_equal(f, r.forces) and t == r.etotal
+
+
+@pytest.mark.parametrize("cells", [(10, 10, 10), (16, 16, 16), (3, 3, 3)])
+def test_y_to_de_overlap_bitwise(snap, cells):
+    """The per-tile compute_Y -> compute_fused_dE hand-off (dE CTAs start on
+    a tile's flag while other tiles still run) gives bitwise the results of
+    waiting for the whole compute_Y grid, run after run, and through the
+    one-call path; the automatic plan (tiles with one part more) stays
+    within round-off of the uniform two-part split."""
+    p = snap.bcc_problem(*cells, twojmax=8)
+    with snap.SnapEngine.for_problem(p) as eng:
+        eng.set_problem(p)
+        eng.set_overlap(False)
+        eng.run()
+        f0, (e0, t0) = eng.forces().copy(), eng.energy()
+        d0 = eng.dedr()
+        eng.set_overlap(True)
+        for _ in range(5):
+            eng.run()
+            assert np.array_equal(eng.forces(), f0) and np.array_equal(eng.dedr(), d0)
+            e1, t1 = eng.energy()
+            assert np.array_equal(e1, e0) and t1 == t0
+        f2, e2, t2 = eng.step(p.numneigh, p.nbr, p.disp)
+        assert np.array_equal(f2, f0) and t2 == t0
+        eng.tune(2)
+        eng.run()
+        f3 = eng.forces()
+        assert np.abs(f3 - f0).max() <= 1e-12 * np.abs(f0).max()
