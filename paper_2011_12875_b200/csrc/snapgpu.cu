@@ -653,7 +653,12 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
     c->hf = half_f(c->maps);
     c->ywgt = half_ywgt(c->maps);
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    {  // the reverse-index build runs beside compute_Y, which fills every SM:
+       // its small kernels take SMs ahead of the waiting compute_fused_dE CTAs
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, hi));
+    }
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->stream = c->own_stream;
