@@ -479,7 +479,10 @@ struct U2Cfg {
   static constexpr int NC = T + 1;
   static constexpr int NACC = (T + 1) * (T + 2) / 2;  // (t, c) of one row, all levels
   static constexpr int NH = c_half_off(T + 1);
-  static constexpr int WARPS = 4;
+#ifndef SNAP_U2_WARPS
+#define SNAP_U2_WARPS 1  // one-warp CTAs spread the warps evenly over the SMs (262k atoms: U 1.393 -> 1.340 ms)
+#endif
+  static constexpr int WARPS = SNAP_U2_WARPS;
 };
 
 template <int T, int SL, int PP>
