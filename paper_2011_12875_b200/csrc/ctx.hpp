@@ -106,12 +106,15 @@ struct snapgpu_ctx {
   int y_parts_max = 1;    // the most parts any tile has in the current plan
   int y_ctas = 0;         // compute_Y grid (2J <= 8): one CTA per (tile, part)
   snapgpu::host::DevBuf<int4> d_ycta;    // per CTA {tile, part | parts << 8, row list, stride}
-  snapgpu::host::DevBuf<unsigned> d_ready;  // [ntiles] tile flags + [1] etotal flag (Y -> dE)
+  snapgpu::host::DevBuf<unsigned> d_ready;  // [ntiles] tile flags (Y -> dE hand-off)
   // compute_fused_dE starts per tile while compute_Y still runs (2J <= 8).
   // Off when a tool is injected (ncu: CUDA_INJECTION64_PATH, compute-
   // sanitizer: NV_SANITIZER_INJECTION_*): tools may serialize the grids, and
   // a dE CTA waiting for a tile would then wait for a CTA that cannot run.
   bool y_overlap = true;
+  // the hand-off in use: on, and a single force chunk (the chunked multi-GPU
+  // layout copies compute_Y's etotal in the gather, after the grid-wide wait)
+  bool overlap_now() const { return y_overlap && nchunks == 1; }
 
   // problem shape
   int natoms_total = 0, atom_lo = 0, nlocal = 0, stride = 0, ntiles = 0;
@@ -163,6 +166,15 @@ struct snapgpu_ctx {
   }
   int chunk_stride() const { return nchunks > 1 ? 3 * chunk_rows() + 1 : 3 * chunk_rows(); }
 
+  // the one-call pull step (pinned lists and outputs) as a graph; the host
+  // pointers of each call are patched into its U / Y / gather nodes
+  cudaGraph_t pull_graph = nullptr;
+  cudaGraphExec_t pull_gexec = nullptr;
+  cudaGraphNode_t pull_node[3] = {nullptr, nullptr, nullptr};  // U, Y, gather
+  cudaKernelNodeParams pull_kp[3] = {};
+  snapgpu::UArgs pull_u{};
+  snapgpu::YWArgs pull_y{};
+  alignas(16) unsigned char pull_g[256];  // the GatherArgs (host translation unit only)
   // graphs: the force step, and the reverse-index build
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -239,7 +251,6 @@ inline EnergyOut energy_out(snapgpu_ctx* c) {
   E.etotal_host = c->sink_etotal;
   E.pstride = c->y_parts_max;
   E.ready = nullptr;  // set by the 2J <= 8 compute_Y launch
-  E.done = nullptr;
   return E;
 }
 

@@ -752,10 +752,9 @@ struct EnergyOut {
   double* etotal_host;
   // compute_Y -> compute_fused_dE hand-off per 32-atom tile (2J <= 8; null
   // otherwise): ready[tile] = 1 once every part of the tile wrote its Y'
-  // rows, *done = 1 once etotal is final.  Reset by each tile's part 0 at
-  // its start (before the CTA lets the dependents launch).
+  // rows.  Reset by each tile's part 0 at its start (before the CTA lets
+  // the dependents launch).
   unsigned* ready;
-  unsigned* done;
 };
 
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
@@ -808,10 +807,6 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
   if (lane == 0) {
     *E.etotal = acc;
     if (E.etotal_host) *E.etotal_host = acc;
-    if (E.done) {
-      __threadfence();
-      st_release(E.done, 1u);
-    }
     *E.ticket = 0u;
   }
 }
@@ -1391,7 +1386,6 @@ __global__ void __launch_bounds__(kYWarps * 32, 1) k_compute_Y_cwin(const YWArgs
   const int tile = ci.x, part = ci.y & 0xff, parts = ci.y >> 8;
   if (part == 0 && threadIdx.x == 0 && A.E.ready) {  // this step's hand-off starts empty
     A.E.ready[tile] = 0u;
-    if (tile == 0) *A.E.done = 0u;
     __threadfence();
   }
   const double* Vt = A.V + (size_t)tile * 2 * NH * 32;
@@ -1908,7 +1902,6 @@ struct GatherArgs {
   double* forces;
   int chunk_rows, chunk_stride, nchunks;
   const double* etotal;  // this rank's total (nchunks > 1)
-  const unsigned* ydone; // compute_Y's "etotal final" flag (2J <= 8), else null
   unsigned* flags_out;   // the validation flags copied here (one-call read-back slot)
   // optional second sinks (mapped host memory of the one-call step)
   double* forces_host;   // [natoms][3] (single chunk only)
@@ -1927,9 +1920,7 @@ __global__ void __launch_bounds__(128) k_gather_forces(const GatherArgs A) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int a = t / 3, d = t - 3 * (t / 3);
   if (A.nchunks > 1 && t < A.nchunks) {  // this rank's energy into every chunk's slot
-    pdl_wait();                           // (etotal comes from compute_Y)
-    if (A.ydone)  // compute_fused_dE no longer waits for compute_Y's end
-      while (ld_acquire(A.ydone) == 0u) __nanosleep(200);
+    pdl_wait();  // (etotal comes from compute_Y; the chunked layout keeps the grid-wide Y -> dE wait)
     A.forces[(size_t)t * A.chunk_stride + 3 * (size_t)A.chunk_rows] = __ldcg(A.etotal);
   }
   if (t == 0) {  // final after compute_U

@@ -109,11 +109,10 @@ void launch_Y_t(snapgpu_ctx* c) {
   a.tasks = c->d_tasks.p;
   a.cta = c->d_ycta.p;
   a.ntiles = c->ntiles;
-  a.early = c->y_overlap ? 1 : 0;
+  a.early = c->overlap_now() ? 1 : 0;
   a.nlocal = c->nlocal;
   a.E = energy_out(c);
   a.E.ready = c->d_ready.p;  // the per-tile hand-off to compute_fused_dE
-  a.E.done = c->d_ready.p + c->ntiles;
   const size_t smem = sizeof(double) * (2 * NP * 32 + (size_t)kYRedSlots * (T + 1) * 2 * 32 +
                                         (size_t)c_cwp_total(T));
   dim3 grid(c->y_ctas);
@@ -177,7 +176,7 @@ void launch_DE_t(snapgpu_ctx* c) {
   a.dedr = c->d_dedr.p;
   a.nslots = c->nlocal * c->stride;
   // 2J <= 8: wait per tile on compute_Y's flags instead of for its whole grid
-  a.ready = (T <= SNAP_CWIN_MAXT && c->y_overlap) ? c->d_ready.p : nullptr;
+  a.ready = (T <= SNAP_CWIN_MAXT && c->overlap_now()) ? c->d_ready.p : nullptr;
   const int per_block = R::WARPS * R::PPW;
   const int blocks = (a.nslots + per_block - 1) / per_block;
   if (blocks > 0) {

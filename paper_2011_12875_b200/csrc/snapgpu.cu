@@ -23,6 +23,10 @@ void invalidate_graph(snapgpu_ctx* c) {
   if (c->fork_graph) cudaGraphDestroy(c->fork_graph);
   c->fork_gexec = nullptr;
   c->fork_graph = nullptr;
+  if (c->pull_gexec) cudaGraphExecDestroy(c->pull_gexec);
+  if (c->pull_graph) cudaGraphDestroy(c->pull_graph);
+  c->pull_gexec = nullptr;
+  c->pull_graph = nullptr;
 }
 
 void invalidate_pos_graph(snapgpu_ctx* c) {
@@ -133,8 +137,8 @@ void plan_y(snapgpu_ctx* c) {
     CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
     c->d_ycta.alloc(cta.size());
     CK(cudaMemcpy(c->d_ycta.p, cta.data(), cta.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    c->d_ready.alloc((size_t)ntiles + 1);
-    CK(cudaMemsetAsync(c->d_ready.p, 0, sizeof(unsigned) * ((size_t)ntiles + 1), c->stream));
+    c->d_ready.alloc((size_t)ntiles);
+    CK(cudaMemsetAsync(c->d_ready.p, 0, sizeof(unsigned) * (size_t)ntiles, c->stream));
   } else if (c->y_parts > 0) {
     pmax = c->y_parts;
   }
@@ -312,8 +316,6 @@ void launch_gather(snapgpu_ctx* c) {
   a.chunk_stride = c->chunk_stride();
   a.nchunks = c->nchunks;
   a.etotal = c->d_etotal.p;
-  a.ydone = (c->T <= SNAP_CWIN_MAXT && c->y_overlap && c->d_ready.p)
-                ? c->d_ready.p + std::max(1, c->ntiles) : nullptr;
   a.flags_out = reinterpret_cast<unsigned*>(c->d_out.p + c->d_forces.n + c->d_eatom.n + 1);
   a.forces_host = c->sink_forces;
   a.flags_host = c->sink_flags;
@@ -559,6 +561,88 @@ void run_pull(snapgpu_ctx* c, const int* nn, const int* nb, const double* dp) {
     c->zc_disp = nullptr;
     throw;
   }
+  c->csr_dirty = false;
+}
+
+// The node the capture on `s` just added (its single current dependency).
+cudaGraphNode_t last_node(cudaStream_t s) {
+  cudaStreamCaptureStatus st;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &nd));
+  if (st != cudaStreamCaptureStatusActive || nd != 1) throw CudaError{"pull graph: capture state"};
+  return deps[0];
+}
+
+// run_pull as one graph (pinned lists and pinned outputs): captured once per
+// shape, then each call patches its host pointers into the U node (list
+// sources), the Y node (eatom / etotal sinks) and the gather node (forces /
+// flags sinks) and replays it -- no per-kernel launch overhead, no gaps.
+void run_pull_graph(snapgpu_ctx* c, const int* nn, const int* nb, const double* dp) {
+  if (!c->pull_gexec) {
+    cudaStream_t user = c->stream;
+    c->stream = c->own_stream;
+    CK(cudaStreamSynchronize(user));
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      c->zc_numneigh = nn;
+      c->zc_nbr = nb;
+      c->zc_disp = dp;
+      launch_U(c);
+      c->pull_node[0] = last_node(c->stream);
+      c->zc_numneigh = c->zc_nbr = nullptr;
+      c->zc_disp = nullptr;
+      CK(cudaEventRecord(c->ev_fork, c->own_stream));
+      CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+      c->stream = c->side_stream;
+      launch_rev_build(c);
+      CK(cudaEventRecord(c->ev_join, c->side_stream));
+      c->stream = c->own_stream;
+      launch_Y(c);
+      c->pull_node[1] = last_node(c->stream);
+      launch_dE(c);
+      CK(cudaStreamWaitEvent(c->own_stream, c->ev_join, 0));
+      launch_gather(c);
+      c->pull_node[2] = last_node(c->stream);
+    } catch (...) {
+      c->stream = c->own_stream;
+      c->zc_numneigh = c->zc_nbr = nullptr;
+      c->zc_disp = nullptr;
+      cudaGraph_t g;
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c->stream = user;
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &c->pull_graph));
+    CK(cudaGraphInstantiate(&c->pull_gexec, c->pull_graph, 0));
+    c->stream = user;
+    for (int k = 0; k < 3; ++k) CK(cudaGraphKernelNodeGetParams(c->pull_node[k], &c->pull_kp[k]));
+    std::memcpy(&c->pull_u, c->pull_kp[0].kernelParams[0], sizeof(UArgs));
+    std::memcpy(&c->pull_y, c->pull_kp[1].kernelParams[0], sizeof(YWArgs));
+    static_assert(sizeof(GatherArgs) <= sizeof(c->pull_g), "pull graph: gather args storage");
+    std::memcpy(c->pull_g, c->pull_kp[2].kernelParams[0], sizeof(GatherArgs));
+  }
+  UArgs u = c->pull_u;
+  u.src_numneigh = nn;
+  u.src_nbr = nb;
+  u.src_disp = dp;
+  YWArgs y = c->pull_y;
+  y.E.eatom_host = c->sink_eatom;
+  y.E.etotal_host = c->sink_etotal;
+  GatherArgs g;
+  std::memcpy(&g, c->pull_g, sizeof(GatherArgs));
+  g.forces_host = c->sink_forces;
+  g.flags_host = c->sink_flags;
+  void* pu[1] = {&u};
+  void* py[1] = {&y};
+  void* pg[1] = {&g};
+  cudaKernelNodeParams kp[3] = {c->pull_kp[0], c->pull_kp[1], c->pull_kp[2]};
+  kp[0].kernelParams = pu;
+  kp[1].kernelParams = py;
+  kp[2].kernelParams = pg;
+  for (int k = 0; k < 3; ++k) CK(cudaGraphExecKernelNodeSetParams(c->pull_gexec, c->pull_node[k], &kp[k]));
+  CK(cudaGraphLaunch(c->pull_gexec, c->stream));
   c->csr_dirty = false;
 }
 
@@ -978,8 +1062,12 @@ int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, 
         }
       }
       try {
-        run_pull(c, static_cast<const int*>(zn), static_cast<const int*>(zb),
-                 static_cast<const double*>(zd));
+        if (sunk && c->T <= SNAP_CWIN_MAXT)
+          run_pull_graph(c, static_cast<const int*>(zn), static_cast<const int*>(zb),
+                         static_cast<const double*>(zd));
+        else
+          run_pull(c, static_cast<const int*>(zn), static_cast<const int*>(zb),
+                   static_cast<const double*>(zd));
       } catch (...) {
         c->sink_forces = c->sink_eatom = c->sink_etotal = nullptr;
         c->sink_flags = nullptr;

@@ -8,6 +8,10 @@ import numpy as np  # noqa: E402
 import paper_2011_12875_b200 as snap  # noqa: E402
 
 
+def log(*a):
+    print("sanitize_step:", *a, flush=True)
+
+
 def exercise(p, parts=(0,)):
     with snap.SnapEngine.for_problem(p) as eng:
         eng.set_problem(p)
@@ -16,12 +20,17 @@ def exercise(p, parts=(0,)):
         eng.compute_fused_dE()
         eng.scatter_forces()
         f = eng.forces()
+        log("staged")
         for yp in parts:
             eng.tune(y_parts=yp)
             eng.run()
+            eng.synchronize()
+            log("graph run, y_parts", yp)
         eng.virial()
         eng.descriptors()
+        log("virial, descriptors")
         f2, e, t = eng.step(p.numneigh, p.nbr, p.disp)
+        log("one-call step")
         assert np.isfinite(f).all() and np.isfinite(f2).all() and np.isfinite(t)
         if p.positions is not None:
             eng.set_positions(p.positions, p.box)
