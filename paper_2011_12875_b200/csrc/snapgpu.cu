@@ -623,25 +623,31 @@ void run_pull_graph(snapgpu_ctx* c, const int* nn, const int* nb, const double* 
     static_assert(sizeof(GatherArgs) <= sizeof(c->pull_g), "pull graph: gather args storage");
     std::memcpy(c->pull_g, c->pull_kp[2].kernelParams[0], sizeof(GatherArgs));
   }
-  UArgs u = c->pull_u;
+  // patch the nodes whose host pointers differ from the last replay (an MD
+  // loop passes the same pinned buffers every step: no patch at all)
+  UArgs& u = c->pull_u;
+  YWArgs& y = c->pull_y;
+  GatherArgs g;
+  std::memcpy(&g, c->pull_g, sizeof(GatherArgs));
+  const bool du = u.src_numneigh != nn || u.src_nbr != nb || u.src_disp != dp;
+  const bool dy = y.E.eatom_host != c->sink_eatom || y.E.etotal_host != c->sink_etotal;
+  const bool dg = g.forces_host != c->sink_forces || g.flags_host != c->sink_flags;
   u.src_numneigh = nn;
   u.src_nbr = nb;
   u.src_disp = dp;
-  YWArgs y = c->pull_y;
   y.E.eatom_host = c->sink_eatom;
   y.E.etotal_host = c->sink_etotal;
-  GatherArgs g;
-  std::memcpy(&g, c->pull_g, sizeof(GatherArgs));
   g.forces_host = c->sink_forces;
   g.flags_host = c->sink_flags;
-  void* pu[1] = {&u};
-  void* py[1] = {&y};
-  void* pg[1] = {&g};
-  cudaKernelNodeParams kp[3] = {c->pull_kp[0], c->pull_kp[1], c->pull_kp[2]};
-  kp[0].kernelParams = pu;
-  kp[1].kernelParams = py;
-  kp[2].kernelParams = pg;
-  for (int k = 0; k < 3; ++k) CK(cudaGraphExecKernelNodeSetParams(c->pull_gexec, c->pull_node[k], &kp[k]));
+  std::memcpy(c->pull_g, &g, sizeof(GatherArgs));
+  void* pp[3] = {&u, &y, &g};
+  const bool dirty[3] = {du, dy, dg};
+  for (int k = 0; k < 3; ++k) {
+    if (!dirty[k]) continue;
+    cudaKernelNodeParams kp = c->pull_kp[k];
+    kp.kernelParams = &pp[k];
+    CK(cudaGraphExecKernelNodeSetParams(c->pull_gexec, c->pull_node[k], &kp));
+  }
   CK(cudaGraphLaunch(c->pull_gexec, c->stream));
   c->csr_dirty = false;
 }
