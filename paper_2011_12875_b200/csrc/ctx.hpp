@@ -175,6 +175,17 @@ struct snapgpu_ctx {
   snapgpu::UArgs pull_u{};
   snapgpu::YWArgs pull_y{};
   alignas(16) unsigned char pull_g[256];  // the GatherArgs (host translation unit only)
+  // the one-call positions step with pinned positions and outputs: the
+  // binning kernel reads the positions from host memory, the kernels write
+  // the results into the outputs; per-call pointers patched into its
+  // binning / Y / gather nodes
+  cudaGraph_t ppos_graph = nullptr;
+  cudaGraphExec_t ppos_gexec = nullptr;
+  cudaGraphNode_t ppos_node[3] = {nullptr, nullptr, nullptr};  // bin, Y, gather
+  cudaKernelNodeParams ppos_kp[3] = {};
+  alignas(16) unsigned char ppos_nl[256];  // the NLArgs (host translation unit only)
+  snapgpu::YWArgs ppos_y{};
+  alignas(16) unsigned char ppos_g[256];
   // graphs: the force step, and the reverse-index build
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;

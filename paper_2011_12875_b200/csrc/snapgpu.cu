@@ -34,6 +34,10 @@ void invalidate_pos_graph(snapgpu_ctx* c) {
   if (c->pos_graph) cudaGraphDestroy(c->pos_graph);
   c->pos_gexec = nullptr;
   c->pos_graph = nullptr;
+  if (c->ppos_gexec) cudaGraphExecDestroy(c->ppos_gexec);
+  if (c->ppos_graph) cudaGraphDestroy(c->ppos_graph);
+  c->ppos_gexec = nullptr;
+  c->ppos_graph = nullptr;
 }
 
 template <class F>
@@ -652,6 +656,88 @@ void run_pull_graph(snapgpu_ctx* c, const int* nn, const int* nb, const double* 
   c->csr_dirty = false;
 }
 
+// The one-call positions step from pinned positions into pinned outputs
+// (host pointers already device-mapped; sinks set by the caller): binning
+// reads the positions over PCIe, lists, partner slots, U, Y, dE, gather with
+// the result sinks -- one graph, no copies; per-call pointers patched into
+// the binning, Y and gather nodes when they change.
+void run_positions_pull(snapgpu_ctx* c, int natoms, const double* pos) {
+  if (!c->ppos_gexec) {
+    cudaStream_t user = c->stream;
+    c->stream = c->own_stream;
+    CK(cudaStreamSynchronize(user));
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      NLArgs a = nl_setup(c, natoms, pos, c->nl_box);
+      a.pos = pos;  // mapped host positions (the binning kernel's only input)
+      const long ncell = a.cells ? (long)a.nc[0] * a.nc[1] * a.nc[2] : 0;
+      CK(cudaMemsetAsync(a.head, 0, sizeof(int) * (ncell + 1), c->stream));
+      const int blk = (a.n + 127) / 128;
+      k_nl_bin<<<blk, 128, 0, c->stream>>>(a);
+      CK(cudaGetLastError());
+      c->ppos_node[0] = last_node(c->stream);
+      if (a.cells) {
+        k_nl_scan<<<1, 1024, 0, c->stream>>>(a.head, (int)ncell, a.fill);
+        k_nl_members<<<blk, 128, 0, c->stream>>>(a);
+      }
+      a.numneigh = c->d_numneigh.p;
+      a.nbr = c->d_nbr.p;
+      a.disp = c->d_disp.p;
+      a.stride = c->stride;
+      a.maxcount = nullptr;
+      k_nl_lists_warp<<<(natoms + kNLWarps - 1) / kNLWarps, kNLWarps * 32, 0, c->stream>>>(
+          a, c->d_err.p);
+      CK(cudaGetLastError());
+      launch_partner(c);
+      launch_U(c);
+      launch_Y(c);
+      c->ppos_node[1] = last_node(c->stream);
+      launch_dE(c);
+      launch_gather(c);
+      c->ppos_node[2] = last_node(c->stream);
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c->stream = user;
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &c->ppos_graph));
+    CK(cudaGraphInstantiate(&c->ppos_gexec, c->ppos_graph, 0));
+    c->stream = user;
+    for (int k = 0; k < 3; ++k) CK(cudaGraphKernelNodeGetParams(c->ppos_node[k], &c->ppos_kp[k]));
+    static_assert(sizeof(NLArgs) <= sizeof(c->ppos_nl), "positions graph: binning args storage");
+    std::memcpy(c->ppos_nl, c->ppos_kp[0].kernelParams[0], sizeof(NLArgs));
+    std::memcpy(&c->ppos_y, c->ppos_kp[1].kernelParams[0], sizeof(YWArgs));
+    static_assert(sizeof(GatherArgs) <= sizeof(c->ppos_g), "positions graph: gather args storage");
+    std::memcpy(c->ppos_g, c->ppos_kp[2].kernelParams[0], sizeof(GatherArgs));
+  }
+  NLArgs a;
+  std::memcpy(&a, c->ppos_nl, sizeof(NLArgs));
+  YWArgs& y = c->ppos_y;
+  GatherArgs g;
+  std::memcpy(&g, c->ppos_g, sizeof(GatherArgs));
+  const bool da = a.pos != pos;
+  const bool dy = y.E.eatom_host != c->sink_eatom || y.E.etotal_host != c->sink_etotal;
+  const bool dg = g.forces_host != c->sink_forces || g.flags_host != c->sink_flags;
+  a.pos = pos;
+  y.E.eatom_host = c->sink_eatom;
+  y.E.etotal_host = c->sink_etotal;
+  g.forces_host = c->sink_forces;
+  g.flags_host = c->sink_flags;
+  std::memcpy(c->ppos_g, &g, sizeof(GatherArgs));
+  std::memcpy(c->ppos_nl, &a, sizeof(NLArgs));
+  void* pp[3] = {&a, &y, &g};
+  const bool dirty[3] = {da, dy, dg};
+  for (int k = 0; k < 3; ++k) {
+    if (!dirty[k]) continue;
+    cudaKernelNodeParams kp = c->ppos_kp[k];
+    kp.kernelParams = &pp[k];
+    CK(cudaGraphExecKernelNodeSetParams(c->ppos_gexec, c->ppos_node[k], &kp));
+  }
+  CK(cudaGraphLaunch(c->ppos_gexec, c->stream));
+}
+
 void run_direct(snapgpu_ctx* c) {
   record(c, 0);
   launch_U(c);
@@ -1265,6 +1351,9 @@ int snapgpu_set_positions(snapgpu_ctx* c, int natoms, const double* pos, const d
     // partner slots instead of a reverse-neighbor CSR
     c->sym_lists = true;
     c->csr_dirty = false;
+    // the positions graphs embed the box (cells, minimum image)
+    if (box[0] != c->nl_box[0] || box[1] != c->nl_box[1] || box[2] != c->nl_box[2])
+      invalidate_pos_graph(c);
     for (int d = 0; d < 3; ++d) c->nl_box[d] = box[d];
   });
 }
@@ -1282,7 +1371,53 @@ int snapgpu_run_positions(snapgpu_ctx* c, int natoms, const double* pos, const d
       const int rc = snapgpu_set_positions(c, natoms, pos, box);
       if (rc != SNAPGPU_OK) return rc;
     }
-    bool overflow = false;
+    bool overflow = false, done = false;
+    // pinned positions and outputs (2J <= 8): the copy-free graph
+    const int rp = guarded(c, [&] {
+      require(natoms > 0, "run_positions: no atoms");
+      if (c->T > SNAP_CWIN_MAXT || c->nchunks != 1 || c->ext_forces) return;
+      const double* mp = static_cast<const double*>(mapped_ptr(pos));
+      double* sf = forces ? static_cast<double*>(const_cast<void*>(mapped_ptr(forces))) : nullptr;
+      double* se = eatom ? static_cast<double*>(const_cast<void*>(mapped_ptr(eatom))) : nullptr;
+      double* st = etotal ? static_cast<double*>(const_cast<void*>(mapped_ptr(etotal))) : nullptr;
+      unsigned* sg = static_cast<unsigned*>(const_cast<void*>(mapped_ptr(c->h_err)));
+      if (!mp || !sg || (forces && !sf) || (eatom && !se) || (etotal && !st)) return;
+      c->sink_forces = sf;
+      c->sink_eatom = se;
+      c->sink_etotal = st;
+      c->sink_flags = sg;
+      try {
+        run_positions_pull(c, natoms, mp);
+      } catch (...) {
+        c->sink_forces = c->sink_eatom = c->sink_etotal = nullptr;
+        c->sink_flags = nullptr;
+        throw;
+      }
+      c->sink_forces = c->sink_eatom = c->sink_etotal = nullptr;
+      c->sink_flags = nullptr;
+      CK(cudaStreamSynchronize(c->stream));
+      c->have_U = c->have_Y = c->have_dE = c->have_forces = true;
+      const unsigned f = *static_cast<volatile unsigned*>(c->h_err);
+      done = true;
+      if (f) {
+        *c->h_err = 0u;
+        CK(cudaMemsetAsync(c->d_err.p, 0, sizeof(unsigned), c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->have_U = c->have_Y = c->have_dE = c->have_forces = false;
+        if ((f & kErrCount) && attempt == 0) {  // a list outgrew the stride: rebuild
+          overflow = true;
+          return;
+        }
+        c->have_lists = false;
+        throw InvalidArg{device_error_message(f)};
+      }
+    });
+    if (rp != SNAPGPU_OK) return rp;
+    if (done && !overflow) return SNAPGPU_OK;
+    if (overflow) {
+      fast = false;
+      continue;
+    }
     const int rc = guarded(c, [&] {
       require(natoms > 0, "run_positions: no atoms");
       const size_t nf = c->d_forces.n, ne = c->d_eatom.n, nout = nf + ne + 2;

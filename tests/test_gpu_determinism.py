@@ -180,3 +180,40 @@ def test_y_to_de_overlap_bitwise(snap, cells):
         eng.run()
         f3 = eng.forces()
         assert np.abs(f3 - f0).max() <= 1e-12 * np.abs(f0).max()
+
+
+def test_positions_step_pinned_and_box_change(snap):
+    """snapgpu_run_positions with pinned positions and outputs (the copy-free
+    graph: binning reads the positions over PCIe, the kernels write the
+    results in place) equals the pageable path bitwise; a box change that
+    keeps the list stride re-plans the graphs (cells, minimum image)."""
+    import torch
+
+    p = snap.bcc_problem(10, 10, 10, twojmax=8)
+    keep = []
+
+    def pin(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        keep.append(t)
+        return t.numpy()
+
+    with snap.SnapEngine.for_problem(p) as eng:
+        f0, e0, t0 = eng.step_positions(p.positions, p.box)
+        pos = pin(p.positions)
+        outs = [pin(np.zeros(x)) for x in ((p.natoms, 3), p.natoms, 1)]
+        for _ in range(3):
+            f1, e1, t1 = eng.step_positions(pos, p.box, *outs)
+            assert np.array_equal(f1, f0) and np.array_equal(e1, e0) and t1 == t0
+        rng = np.random.default_rng(5)
+        q = p.positions + rng.uniform(-0.02, 0.02, p.positions.shape)
+        pos[:] = q
+        f2, _, t2 = eng.step_positions(pos, p.box, *outs)
+        fr, _, tr = eng.step_positions(q, p.box)  # pageable path on the same positions
+        assert np.array_equal(f2, fr) and t2 == tr
+        box2 = p.box * 1.002  # same neighbor count, new cells / minimum image
+        f3, _, t3 = eng.step_positions(pos, box2, *outs)
+        nn, nbr, disp = snap.build_neighborlist(q, box2, p.rcut)
+        pr = snap.Problem.from_any(p)
+        pr.numneigh, pr.nbr, pr.disp = nn, nbr, disp
+        r = snap.run_pipeline(pr)
+        assert np.array_equal(f3, r.forces) and t3 == r.etotal
