@@ -2168,8 +2168,8 @@ __global__ void __launch_bounds__(kNLWarps * 32) k_nl_lists_warp(const NLArgs A,
     return r2 < A.rc2;
   };
   // candidates: lane c scans stencil cell c (or, without cells, atoms lane +
-  // 32 q); two passes over the same candidates: count, then write at the
-  // lane's offset (no per-lane buffers)
+  // 32 q); the hits are counted, scanned across the warp and written at the
+  // lane's offset
   int s0 = 0, s1 = 0;
   if (A.cells && lane < 27) {
     const int c = A.cell_of[i];
@@ -2214,8 +2214,17 @@ __global__ void __launch_bounds__(kNLWarps * 32) k_nl_lists_warp(const NLArgs A,
         if (k != i && inside(k)) f(k);
     }
   };
+  // one pass: each lane keeps up to kPer hits of its cell in shared memory
+  // (a second scan only for a warp with a denser cell)
+  constexpr int kPer = 16;
+  __shared__ int sfound[kNLWarps][32][kPer];
   int mine = 0;
-  scan([&](int) { ++mine; });
+  bool over = false;
+  scan([&](int k) {
+    if (mine < kPer) sfound[wl][lane][mine] = k;
+    else over = true;
+    ++mine;
+  });
   int cnt = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {  // inclusive scan of the counts
@@ -2233,7 +2242,11 @@ __global__ void __launch_bounds__(kNLWarps * 32) k_nl_lists_warp(const NLArgs A,
     if (lane == 0) atomicOr(err, kErrCount);
     return;
   }
-  scan([&](int k) { buf[off++] = k; });
+  if (__any_sync(0xffffffffu, over)) {
+    scan([&](int k) { buf[off++] = k; });
+  } else {
+    for (int m = 0; m < mine; ++m) buf[off + m] = sfound[wl][lane][m];
+  }
   __syncwarp();
   // rank sort of the distinct indices, then write in index order
   for (int q = lane; q < total; q += 32) {
