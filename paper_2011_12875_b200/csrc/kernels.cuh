@@ -2145,6 +2145,69 @@ __global__ void k_nl_members(const NLArgs A) {
   A.members[atomicAdd(A.fill + A.cell_of[i], 1)] = i;
 }
 
+// Small systems (one CTA): the zeroing, binning, cell scan and member fill of
+// k_nl_bin / k_nl_scan / k_nl_members in one launch, phases separated by
+// block barriers (the multi-kernel front is launch-bound at 2000 atoms).
+constexpr int kNLSmallAtoms = 16384, kNLSmallCells = 8192;
+__global__ void __launch_bounds__(1024) k_nl_front_small(const NLArgs A) {
+  __shared__ int cnt[kNLSmallCells];  // per-cell counts, then fill cursors
+  __shared__ int wsum[32];
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, w = t >> 5;
+  const int ncell = A.cells ? A.nc[0] * A.nc[1] * A.nc[2] : 0;
+  for (int c = t; c < ncell; c += nt) cnt[c] = 0;
+  __syncthreads();
+  for (int i = t; i < A.n; i += nt) {
+    int ci[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double x = nl_wrap(A.pos[i * 3 + d], A.box[d]);
+      A.w[i * 3 + d] = x;
+      const int idx = (int)__dmul_rn(x, __ddiv_rn((double)A.nc[d], A.box[d]));
+      ci[d] = idx >= A.nc[d] ? A.nc[d] - 1 : idx;
+    }
+    if (A.cells) {
+      const int c = (ci[2] * A.nc[1] + ci[1]) * A.nc[0] + ci[0];
+      A.cell_of[i] = c;
+      atomicAdd(cnt + c, 1);
+    }
+  }
+  __syncthreads();
+  if (!A.cells) return;
+  // exclusive scan of the counts (k_nl_scan's block scan, in shared memory)
+  const int per = (ncell + nt - 1) / nt;
+  const int b = min(ncell, t * per), e = min(ncell, b + per);
+  int sum = 0;
+  for (int c = b; c < e; ++c) sum += cnt[c];
+  int x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += v;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int y = lane < (nt >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += v;
+    }
+    wsum[lane] = y;
+  }
+  __syncthreads();
+  int acc = x - sum + (w > 0 ? wsum[w - 1] : 0);
+  for (int c = b; c < e; ++c) {
+    const int v = cnt[c];
+    A.head[c] = acc;
+    cnt[c] = acc;  // fill cursor
+    acc += v;
+  }
+  if (t == nt - 1) A.head[ncell] = (w > 0 ? wsum[(nt >> 5) - 1] : x);
+  __syncthreads();
+  for (int i = t; i < A.n; i += nt) A.members[atomicAdd(cnt + A.cell_of[i], 1)] = i;
+}
+
 // Warp-per-atom list build (set_positions pass 2 and the sync-free one-call
 // positions step): lane c < 27 scans cell c of the atom's stencil, the hits
 // are compacted into a shared buffer, ranked (neighbor indices are distinct)

@@ -498,6 +498,11 @@ void nl_front(snapgpu_ctx* c, const NLArgs& a, const double* host_pos) {
   if (a.n > 0)
     CK(cudaMemcpyAsync(const_cast<double*>(a.pos), host_pos, sizeof(double) * 3 * a.n,
                        cudaMemcpyHostToDevice, c->stream));
+  if (a.n > 0 && a.n <= kNLSmallAtoms && ncell <= kNLSmallCells) {  // one launch
+    k_nl_front_small<<<1, 1024, 0, c->stream>>>(a);
+    CK(cudaGetLastError());
+    return;
+  }
   CK(cudaMemsetAsync(a.head, 0, sizeof(int) * (ncell + 1), c->stream));
   const int blk = (a.n + 127) / 128;
   if (a.n > 0) {
@@ -671,14 +676,20 @@ void run_positions_pull(snapgpu_ctx* c, int natoms, const double* pos) {
       NLArgs a = nl_setup(c, natoms, pos, c->nl_box);
       a.pos = pos;  // mapped host positions (the binning kernel's only input)
       const long ncell = a.cells ? (long)a.nc[0] * a.nc[1] * a.nc[2] : 0;
-      CK(cudaMemsetAsync(a.head, 0, sizeof(int) * (ncell + 1), c->stream));
-      const int blk = (a.n + 127) / 128;
-      k_nl_bin<<<blk, 128, 0, c->stream>>>(a);
-      CK(cudaGetLastError());
-      c->ppos_node[0] = last_node(c->stream);
-      if (a.cells) {
-        k_nl_scan<<<1, 1024, 0, c->stream>>>(a.head, (int)ncell, a.fill);
-        k_nl_members<<<blk, 128, 0, c->stream>>>(a);
+      if (a.n <= kNLSmallAtoms && ncell <= kNLSmallCells) {
+        k_nl_front_small<<<1, 1024, 0, c->stream>>>(a);
+        CK(cudaGetLastError());
+        c->ppos_node[0] = last_node(c->stream);
+      } else {
+        CK(cudaMemsetAsync(a.head, 0, sizeof(int) * (ncell + 1), c->stream));
+        const int blk = (a.n + 127) / 128;
+        k_nl_bin<<<blk, 128, 0, c->stream>>>(a);
+        CK(cudaGetLastError());
+        c->ppos_node[0] = last_node(c->stream);
+        if (a.cells) {
+          k_nl_scan<<<1, 1024, 0, c->stream>>>(a.head, (int)ncell, a.fill);
+          k_nl_members<<<blk, 128, 0, c->stream>>>(a);
+        }
       }
       a.numneigh = c->d_numneigh.p;
       a.nbr = c->d_nbr.p;
