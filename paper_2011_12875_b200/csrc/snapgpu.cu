@@ -699,14 +699,22 @@ void run_positions_pull(snapgpu_ctx* c, int natoms, const double* pos) {
       k_nl_lists_warp<<<(natoms + kNLWarps - 1) / kNLWarps, kNLWarps * 32, 0, c->stream>>>(
           a, c->d_err.p);
       CK(cudaGetLastError());
+      // the partner slots only feed the gather: built beside U / Y / dE
+      CK(cudaEventRecord(c->ev_fork, c->stream));
+      CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+      c->stream = c->side_stream;
       launch_partner(c);
+      CK(cudaEventRecord(c->ev_join, c->side_stream));
+      c->stream = c->own_stream;
       launch_U(c);
       launch_Y(c);
       c->ppos_node[1] = last_node(c->stream);
       launch_dE(c);
+      CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
       launch_gather(c);
       c->ppos_node[2] = last_node(c->stream);
     } catch (...) {
+      c->stream = c->own_stream;
       cudaGraph_t g;
       cudaStreamEndCapture(c->stream, &g);
       if (g) cudaGraphDestroy(g);
