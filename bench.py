@@ -402,9 +402,8 @@ def run_ours(args):
         def e2e_step():
             if n_gpus == 1:  # the public one-call API: upload, run, read back
                 eng.step(*host_np, forces=f_host, eatom=e_host, etotal=t_host)
-            else:  # upload the owned lists, step (+ reduce-scatter), read the chunk
-                pe.upload(*host_np)
-                pe.step()
+            else:  # the slab's lists in (read by compute_U), step, reduce-scatter, chunk out
+                pe.step_host(*host_np)
                 c_host.copy_(pe.chunk, non_blocking=True)
                 stream.synchronize()
 

@@ -345,10 +345,12 @@ class SnapEngine:
         self._c(self._L.snapgpu_run(self._h))
 
     def step(self, numneigh, nbr, disp, types=None, forces=None, eatom=None, etotal=None,
-             natoms_total=None, atom_lo=0):
+             natoms_total=None, atom_lo=0, readback=True):
         """One end-to-end force step from host arrays (snapgpu_run_host): upload,
         run, read back; outputs are written into the given (ideally pinned)
-        arrays when provided.  Returns (forces, eatom, etotal)."""
+        arrays when provided.  Returns (forces, eatom, etotal).  With
+        readback=False nothing is read back (the results stay on the device,
+        e.g. for the partitioned step's reduce-scatter) and None is returned."""
         nn = np.ascontiguousarray(numneigh, np.int32)
         nb = np.ascontiguousarray(nbr, np.int32)
         dp = np.ascontiguousarray(disp, np.float64)
@@ -356,6 +358,13 @@ class SnapEngine:
         n = int(nn.shape[0])
         stride = int(nb.shape[1]) if nb.ndim == 2 else int(nb.size // max(n, 1))
         ntot = n if natoms_total is None else int(natoms_total)
+        if not readback:
+            self._c(self._L.snapgpu_run_host(self._h, ntot, int(atom_lo), n, stride,
+                                             nn.ctypes.data, nb.ctypes.data, dp.ctypes.data,
+                                             _ptr(ty), None, None, None))
+            self.natoms_total, self.nlocal, self.stride = ntot, n, stride
+            self._keep = (nn, nb, dp, ty)
+            return None
         f = forces if forces is not None else np.zeros((ntot, 3), np.float64)
         e = eatom if eatom is not None else np.zeros(n, np.float64)
         t = etotal if etotal is not None else np.zeros(1, np.float64)

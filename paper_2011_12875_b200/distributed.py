@@ -146,5 +146,19 @@ class PartitionedEngine:
                 reduce_chunks(self.f_part, self.world, self.rank, out=self.chunk)
         return self.f_own, self.e_tot
 
+    def step_host(self, numneigh, nbr, disp):
+        """One force step from this rank's host lists (the end-to-end call):
+        snapgpu_run_host on the slab -- page-locked lists are read by
+        compute_U over PCIe, validated on the device -- then the
+        reduce-scatter; returns like step()."""
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            self.eng.step(numneigh, nbr, disp, self.types, natoms_total=self.natoms,
+                          atom_lo=self.lo, forces=None, eatom=None, etotal=None, readback=False)
+            if self.world > 1:
+                reduce_chunks(self.f_part, self.world, self.rank, out=self.chunk)
+        return self.f_own, self.e_tot
+
     def close(self):
         self.eng.close()

@@ -29,7 +29,15 @@ def test_gpus_flag_spawns_ranks():
                           "--dry-run", "--config", "C5"], capture_output=True, text=True,
                          timeout=300, env=_env(), cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
-    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    # the two ranks share stdout: their lines may interleave, so decode every
+    # JSON object in the stream rather than line by line
+    dec, text, lines, pos = json.JSONDecoder(), out.stdout, [], 0
+    while True:
+        pos = text.find("{", pos)
+        if pos < 0:
+            break
+        obj, pos = dec.raw_decode(text, pos)
+        lines.append(obj)
     assert sorted(l["rank"] for l in lines) == [0, 1]
     assert all(l["world"] == 2 for l in lines)
     assert lines[0]["config"]["natoms_total"] == 2 * 262144
@@ -53,7 +61,15 @@ def test_reference_arm_is_the_reference_only():
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                          timeout=600, env=_env(), cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
-    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    # the two ranks share stdout: their lines may interleave, so decode every
+    # JSON object in the stream rather than line by line
+    dec, text, lines, pos = json.JSONDecoder(), out.stdout, [], 0
+    while True:
+        pos = text.find("{", pos)
+        if pos < 0:
+            break
+        obj, pos = dec.raw_decode(text, pos)
+        lines.append(obj)
     line, probe = lines[0], lines[-1]
     assert line["impl"] == "reference" and line["value"] > 0
     assert not probe["product_imported"] and not probe["libsnapgpu"] and probe["libsnapref"]

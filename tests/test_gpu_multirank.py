@@ -46,6 +46,14 @@ def _worker(rank, world, port, cells, q):
         for _ in range(2):  # the second step replays the captured graph
             f_own, e_tot = pe.step()
         torch.cuda.synchronize()
+        f_dev, e_dev = f_own.cpu().numpy().copy(), float(e_tot.cpu()[0])
+        # the end-to-end call on pinned host lists (compute_U reads them)
+        pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in pe.own]
+        for _ in range(2):
+            f_own, e_tot = pe.step_host(*[x.numpy() for x in pin])
+        torch.cuda.synchronize()
+        if not (np.array_equal(f_own.cpu().numpy(), f_dev) and float(e_tot.cpu()[0]) == e_dev):
+            raise AssertionError("step_host differs from step")
         q.put((rank, pe.lo, pe.hi, f_own.cpu().numpy().copy(), float(e_tot.cpu()[0])))
         pe.close()
     except Exception as e:  # report instead of hanging the parent
