@@ -732,7 +732,8 @@ __global__ void __launch_bounds__(U2Cfg<T, SL>::WARPS * 32, SNAP_U2_MINB)
 // ---------------------------------------------------------------------------
 // Energy epilogue shared by the compute_Y kernels (replaces compute_energy,
 // snap_core.hpp:684-701), deterministic whatever the launch split: a tile of
-// APT atoms may be spread over `parts` CTAs (grid.y).  Each CTA stores its
+// APT atoms may be spread over `parts` CTAs (k_compute_Y_cwin: a per-tile
+// count from its CTA table; k_compute_Y_quad: grid.y).  Each CTA stores its
 // lane energies in its own slot; the tile's last CTA (ticket) sums the parts
 // in part order into eatom and the tile's energy into tile_sum; the last
 // tile sums tile_sum in tile order into *etotal.  No extra launch, and the
