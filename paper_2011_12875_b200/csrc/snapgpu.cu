@@ -4,6 +4,8 @@
 // from a CUDA graph.
 #include <cstdarg>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys / ncu
+
 #include "ctx.hpp"
 
 using namespace snapgpu;
@@ -12,6 +14,12 @@ using namespace snapgpu::host;
 namespace {
 
 thread_local std::string g_err = "";
+
+// NVTX range over a C-ABI call (a no-op unless a tool is attached)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 void invalidate_graph(snapgpu_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -963,6 +971,7 @@ int snapgpu_set_beta(snapgpu_ctx* c, const double* beta, int nbeta) {
 }
 
 int snapgpu_compute_descriptors(snapgpu_ctx* c, double* blist) {
+  const Nvtx nvtx_range("snapgpu_compute_descriptors");
   if (!c || !blist) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_lists, "compute_descriptors: no neighbor lists");
@@ -1010,6 +1019,7 @@ int snapgpu_set_stream(snapgpu_ctx* c, void* s) {
 
 int snapgpu_set_neighbors(snapgpu_ctx* c, int natoms, int stride, const int* numneigh,
                           const int* nbr, const double* disp, const int* types) {
+  const Nvtx nvtx_range("snapgpu_set_neighbors");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     set_lists(c, natoms, 0, natoms, stride, numneigh, nbr, disp, types);
@@ -1019,6 +1029,7 @@ int snapgpu_set_neighbors(snapgpu_ctx* c, int natoms, int stride, const int* num
 int snapgpu_set_neighbors_partition(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal,
                                     int stride, const int* numneigh, const int* nbr,
                                     const double* disp, const int* types) {
+  const Nvtx nvtx_range("snapgpu_set_neighbors_partition");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     set_lists(c, natoms_total, atom_lo, nlocal, stride, numneigh, nbr, disp, types);
@@ -1026,6 +1037,7 @@ int snapgpu_set_neighbors_partition(snapgpu_ctx* c, int natoms_total, int atom_l
 }
 
 int snapgpu_compute_U(snapgpu_ctx* c) {
+  const Nvtx nvtx_range("snapgpu_compute_U");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_lists, "compute_U needs neighbor lists");
@@ -1036,6 +1048,7 @@ int snapgpu_compute_U(snapgpu_ctx* c) {
 }
 
 int snapgpu_compute_Y(snapgpu_ctx* c) {
+  const Nvtx nvtx_range("snapgpu_compute_Y");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_U, "compute_Y: no Ulisttot");  // snap_core.hpp:1089
@@ -1045,6 +1058,7 @@ int snapgpu_compute_Y(snapgpu_ctx* c) {
 }
 
 int snapgpu_compute_dU_deidrj(snapgpu_ctx* c) {
+  const Nvtx nvtx_range("snapgpu_compute_dU_deidrj");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_Y, "compute_fused_dE: requires Ylist");  // snap_core.hpp:1278
@@ -1054,6 +1068,7 @@ int snapgpu_compute_dU_deidrj(snapgpu_ctx* c) {
 }
 
 int snapgpu_scatter_forces(snapgpu_ctx* c) {
+  const Nvtx nvtx_range("snapgpu_scatter_forces");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_dE, "scatter_forces: no dElist");  // snap_core.hpp:876
@@ -1064,6 +1079,7 @@ int snapgpu_scatter_forces(snapgpu_ctx* c) {
 }
 
 int snapgpu_run(snapgpu_ctx* c) {
+  const Nvtx nvtx_range("snapgpu_run");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     need(c->have_lists, "run: no neighbor lists");
@@ -1139,6 +1155,7 @@ int snapgpu_run(snapgpu_ctx* c) {
 int snapgpu_run_host(snapgpu_ctx* c, int natoms_total, int atom_lo, int nlocal, int stride,
                      const int* numneigh, const int* nbr, const double* disp,
                      const int* types, double* forces, double* eatom, double* etotal) {
+  const Nvtx nvtx_range("snapgpu_run_host");
   if (!c) return SNAPGPU_EINVAL;
   bool pulled = false, sunk = false;
   const int rc = guarded(c, [&] {
@@ -1335,6 +1352,7 @@ int snapgpu_get_ylist(snapgpu_ctx* c, double* out) {
 }
 
 int snapgpu_set_positions(snapgpu_ctx* c, int natoms, const double* pos, const double* box) {
+  const Nvtx nvtx_range("snapgpu_set_positions");
   if (!c) return SNAPGPU_EINVAL;
   return guarded(c, [&] {
     NLArgs a = nl_setup(c, natoms, pos, box);
@@ -1379,6 +1397,7 @@ int snapgpu_set_positions(snapgpu_ctx* c, int natoms, const double* pos, const d
 
 int snapgpu_run_positions(snapgpu_ctx* c, int natoms, const double* pos, const double* box,
                           double* forces, double* eatom, double* etotal) {
+  const Nvtx nvtx_range("snapgpu_run_positions");
   if (!c) return SNAPGPU_EINVAL;
   bool fast = c->have_lists && c->sym_lists && natoms == c->natoms_total &&
               natoms == c->nlocal && c->atom_lo == 0 && c->nchunks == 1 && !c->timing &&
