@@ -230,6 +230,14 @@ int snapgpu_set_force_layout(snapgpu_ctx* ctx, int nchunks, double* ext_forces);
  * z_total_elements, cg_total. */
 int snapgpu_counts(int twojmax, int* out6);
 
+/* Host-only view of the compute_Y launch plan (2J <= 8; no device needed):
+ * for ntiles 32-atom tiles on nsm SMs (y_parts > 0 forces the part count),
+ * writes the CTA table (4 ints per CTA: tile, part | parts << 8, first row
+ * list, list stride) and the row lists (codes j*64+mb, -1 terminated);
+ * returns the CTA count, or a negative status. */
+int snapgpu_debug_y_plan(int twojmax, int ntiles, int nsm, int y_parts, int* cta, int cta_cap,
+                         int* tasks, int tasks_cap);
+
 /* Periodic orthorhombic neighbor lists (harness.hpp:119-202, generalized
  * from cubic): strict r < rcut, minimum image, each list sorted by neighbor
  * index, displacement from center to neighbor.  Returns the maximum

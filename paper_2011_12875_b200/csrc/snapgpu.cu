@@ -104,46 +104,15 @@ void plan_y(snapgpu_ctx* c) {
   if (c->T <= SNAP_CWIN_MAXT) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-    // Parts (CTAs) per 32-atom tile, each taking an LPT share of the tile's
-    // rows.  With fewer tiles than SMs the tiles get floor(nsm / ntiles)
-    // parts and the first nsm mod ntiles tiles one more, so the grid is
-    // exactly one CTA per SM: those tiles finish early and their SMs take
-    // the first compute_fused_dE CTAs (which wait per tile, E.ready) while
-    // the other tiles still run.  snapgpu_tune forces a uniform count.
-    std::vector<int> P(ntiles, 1);
-    if (c->y_parts > 0) {
-      std::fill(P.begin(), P.end(), c->y_parts);
-    } else if (c->ntiles < nsm) {
-      const int base = std::max(1, std::min(kMaxYParts, nsm / ntiles));
-      int extra = base < kMaxYParts ? std::min(ntiles, nsm - base * ntiles) : 0;
-      // an even number of base tiles, so every TPC of the long-running CTAs
-      // pairs the same (parts, part) row lists (see the CTA order below);
-      // an odd group is left to the short extra-part CTAs
-      if (extra > 0 && ((ntiles - extra) & 1)) --extra;
-      for (int t = 0; t < ntiles; ++t) P[t] = base + (t < extra ? 1 : 0);
-    }
-    // one row schedule per distinct part count: parts x kYGroups row lists
-    std::vector<int> tasks;
-    int off[kMaxYParts + 1] = {}, cap[kMaxYParts + 1] = {};
-    for (int q = 1; q <= kMaxYParts; ++q) {
-      if (std::find(P.begin(), P.end(), q) == P.end()) continue;
-      std::vector<int> sched = y_row_schedule(c->maps, c->ycplan.row_cost, q * kYGroups, &cap[q]);
-      off[q] = static_cast<int>(tasks.size());
-      tasks.insert(tasks.end(), sched.begin(), sched.end());
-      pmax = std::max(pmax, q);
-    }
-    // CTA order: by part count (the long-running fewer-part CTAs first), then
-    // part, then tile.  Consecutive CTAs land
-    // on the two SMs of a TPC, which share an instruction cache; CTAs of the
-    // same (parts, part) run the same row lists, hence the same code (tile-
-    // major order made TPC partners run different rows: 2000 atoms, every
-    // row ~1.5x slower).
-    std::vector<int4> cta;
-    for (int q = 1; q <= kMaxYParts; ++q)
-      for (int part = 0; part < q; ++part)
-        for (int t = 0; t < ntiles; ++t)
-          if (P[t] == q)
-            cta.push_back(make_int4(t, part | (q << 8), off[q] + part * kYGroups * cap[q], cap[q]));
+    // per-tile part counts, row lists and the part-major CTA table
+    // (tables.cpp y_cta_plan)
+    const YCtaPlan yp = y_cta_plan(c->maps, c->ycplan.row_cost, ntiles, nsm, c->y_parts,
+                                   kMaxYParts, kYGroups);
+    pmax = yp.pmax;
+    const std::vector<int>& tasks = yp.tasks;
+    std::vector<int4> cta(yp.cta.size());
+    for (size_t k = 0; k < cta.size(); ++k)
+      cta[k] = make_int4(yp.cta[k][0], yp.cta[k][1], yp.cta[k][2], yp.cta[k][3]);
     c->y_ctas = static_cast<int>(cta.size());
     c->d_tasks.alloc(tasks.size());
     CK(cudaMemcpy(c->d_tasks.p, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -800,6 +769,26 @@ const char* snapgpu_last_error(const snapgpu_ctx* c) {
 }
 
 const char* snapgpu_version(void) { return "snapgpu 0.1 (sm_100a, FP64 SIMT, v-space)"; }
+
+int snapgpu_debug_y_plan(int twojmax, int ntiles, int nsm, int y_parts, int* cta, int cta_cap,
+                         int* tasks, int tasks_cap) {
+  int n = 0;
+  const int rc = guarded(nullptr, [&] {
+    require(twojmax >= 0 && twojmax <= SNAP_CWIN_MAXT, "debug_y_plan: twojmax outside [0, 8]");
+    require(ntiles > 0 && nsm > 0 && y_parts >= 0 && y_parts <= kMaxYParts,
+            "debug_y_plan: bad arguments");
+    const IndexMaps m = IndexMaps::build(twojmax);
+    const YCoopPlan cp = ycoop_pair_plan(m, kYGroupWarps);
+    const YCtaPlan yp = y_cta_plan(m, cp.row_cost, ntiles, nsm, y_parts, kMaxYParts, kYGroups);
+    n = static_cast<int>(yp.cta.size());
+    require(cta && cta_cap >= 4 * n && tasks && tasks_cap >= static_cast<int>(yp.tasks.size()),
+            "debug_y_plan: output too small");
+    for (int k = 0; k < n; ++k)
+      for (int q = 0; q < 4; ++q) cta[4 * k + q] = yp.cta[k][q];
+    std::copy(yp.tasks.begin(), yp.tasks.end(), tasks);
+  });
+  return rc == SNAPGPU_OK ? n : rc;
+}
 
 int snapgpu_counts(int twojmax, int* out) {
   return guarded(nullptr, [&] {

@@ -520,6 +520,44 @@ std::vector<int> y_row_schedule(const IndexMaps& m, const std::vector<double>& r
   return out;
 }
 
+// Parts (CTAs) per 32-atom tile, each taking an LPT share of the tile's rows.
+// With fewer tiles than SMs the tiles get floor(nsm / ntiles) parts and the
+// first tiles one more, so the grid is exactly one CTA per SM: those tiles
+// finish early and their SMs take the first compute_fused_dE CTAs (which
+// wait per tile) while the other tiles still run.  The base-count tiles are
+// kept even, so every TPC of the long-running CTAs pairs the same (parts,
+// part) row lists; forced_parts > 0 (snapgpu_tune) gives a uniform count.
+// CTA order: by part count, then part, then tile -- consecutive CTAs land on
+// the two SMs of a TPC, which share an instruction cache, and CTAs of the
+// same (parts, part) run the same row lists, hence the same code.
+YCtaPlan y_cta_plan(const IndexMaps& m, const std::vector<double>& row_cost, int ntiles,
+                    int nsm, int forced_parts, int max_parts, int groups) {
+  YCtaPlan p;
+  ntiles = std::max(1, ntiles);
+  std::vector<int> P(ntiles, 1);
+  if (forced_parts > 0) {
+    std::fill(P.begin(), P.end(), forced_parts);
+  } else if (ntiles < nsm) {
+    const int base = std::max(1, std::min(max_parts, nsm / ntiles));
+    int extra = base < max_parts ? std::min(ntiles, nsm - base * ntiles) : 0;
+    if (extra > 0 && ((ntiles - extra) & 1)) --extra;
+    for (int t = 0; t < ntiles; ++t) P[t] = base + (t < extra ? 1 : 0);
+  }
+  std::vector<int> off(max_parts + 1, 0), cap(max_parts + 1, 0);
+  for (int q = 1; q <= max_parts; ++q) {
+    if (std::find(P.begin(), P.end(), q) == P.end()) continue;
+    std::vector<int> sched = y_row_schedule(m, row_cost, q * groups, &cap[q]);
+    off[q] = static_cast<int>(p.tasks.size());
+    p.tasks.insert(p.tasks.end(), sched.begin(), sched.end());
+    p.pmax = std::max(p.pmax, q);
+  }
+  for (int q = 1; q <= max_parts; ++q)
+    for (int part = 0; part < q; ++part)
+      for (int t = 0; t < ntiles; ++t)
+        if (P[t] == q) p.cta.push_back({t, part | (q << 8), off[q] + part * groups * cap[q], cap[q]});
+  return p;
+}
+
 // ---------------------------------------------------------------------------
 // Neighbor lists: harness.hpp:119-202 arithmetic (wrap_coord :82-86,
 // min_image :88-90, strict r2 < rc2, lists sorted by index), generalized to

@@ -141,6 +141,17 @@ BPlan b_plan(const IndexMaps& m, const std::vector<double>& cg);
 std::vector<int> y_row_schedule(const IndexMaps& m, const std::vector<double>& row_cost,
                                 int workers, int* cap);
 
+// compute_Y (2J <= 8) launch plan: the part count of every 32-atom tile, the
+// per-(parts, part, group) row lists and the CTA table {tile, part | parts <<
+// 8, first row list, list stride} in part-major order (snapgpu.cu plan_y).
+struct YCtaPlan {
+  std::vector<int> tasks;
+  std::vector<std::array<int, 4>> cta;
+  int pmax = 1;
+};
+YCtaPlan y_cta_plan(const IndexMaps& m, const std::vector<double>& row_cost, int ntiles,
+                    int nsm, int forced_parts, int max_parts, int groups);
+
 // Reference-order neighbor list builder (harness.hpp:119-202, orthorhombic).
 // Returns max neighbor count or -1 (err set).
 int build_neighborlist(const double* pos, int n, const double box[3], double rcut,

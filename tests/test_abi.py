@@ -78,3 +78,55 @@ def test_neighborlist_brute_force_random(port):
 def test_no_gpu_fails_loudly():
     with pytest.raises(snap.PipelineError):
         snap.SnapEngine(8, beta=np.zeros(55))
+
+
+def _y_plan(T, ntiles, nsm, parts=0):
+    L = snap.library()
+    cta = np.zeros(4 * 20000, np.int32)
+    tasks = np.zeros(1 << 16, np.int32)
+    fn = L.snapgpu_debug_y_plan
+    fn.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    n = fn(T, ntiles, nsm, parts, cta.ctypes.data, cta.size, tasks.ctypes.data, tasks.size)
+    assert n > 0, snap.library().snapgpu_last_error(None)
+    return cta[: 4 * n].reshape(n, 4), tasks
+
+
+@pytest.mark.parametrize("ntiles", [1, 7, 63, 73, 74, 147, 148, 200, 8192])
+def test_y_launch_plan_covers_every_row_once(ntiles):
+    """compute_Y's launch plan (tables.cpp y_cta_plan): every 32-atom tile
+    is split into parts 0..P-1 exactly once; each (part, group) row list of
+    a tile's part count together covers the tile's 25 target rows (2J=8)
+    exactly once; one wave (CTAs <= SMs) when the tiles are fewer than the
+    SMs, with part counts floor/ceil(SMs / tiles) and an even number of
+    base-count tiles; part-major order (consecutive CTAs share a TPC and run
+    the same row lists)."""
+    nsm, T, groups = 148, 8, 3
+    cta, tasks = _y_plan(T, ntiles, nsm)
+    tile, part, parts = cta[:, 0], cta[:, 1] & 0xFF, cta[:, 1] >> 8
+    rows = sorted(j * 64 + mb for j in range(T + 1) for mb in range(j // 2 + 1))
+    for t in range(ntiles):
+        sel = tile == t
+        P = set(parts[sel])
+        assert len(P) == 1
+        q = P.pop()
+        assert sorted(part[sel]) == list(range(q))
+        got = []
+        for k in np.nonzero(sel)[0]:
+            for g in range(groups):
+                base = cta[k, 2] + g * cta[k, 3]
+                lst = tasks[base: base + cta[k, 3]]
+                got += [int(x) for x in lst[: list(lst).index(-1)]]
+        assert sorted(got) == rows
+    order = list(zip(parts, part, tile))
+    assert order == sorted(order)
+    if ntiles < nsm:
+        assert len(cta) <= nsm
+        base = max(1, min(8, nsm // ntiles))
+        assert set(parts) <= {base, base + 1}
+        if base < 8 and len(set(parts)) == 2:
+            assert (parts[part == 0] == base).sum() % 2 == 0
+    else:
+        assert set(parts) == {1}
+    # a forced part count (snapgpu_tune) is uniform
+    cta2, _ = _y_plan(T, ntiles, nsm, parts=2)
+    assert set(cta2[:, 1] >> 8) == {2} and len(cta2) == 2 * ntiles
