@@ -217,3 +217,24 @@ def test_positions_step_pinned_and_box_change(snap):
         pr.numneigh, pr.nbr, pr.disp = nn, nbr, disp
         r = snap.run_pipeline(pr)
         assert np.array_equal(f3, r.forces) and t3 == r.etotal
+
+
+@pytest.mark.parametrize("n,tune", [(40, 0), (97, 3), (300, 0), (1000, 5)])
+def test_y_to_de_overlap_ragged(snap, port, n, tune):
+    """The per-tile hand-off on ragged typed clusters (a partial last tile,
+    several part counts, forced splits): bitwise the grid-wide wait, and
+    within the parity bar of the oracle."""
+    p = port.make_cluster(n, 8, 1000 + n, ntypes=2)
+    with snap.SnapEngine.for_problem(p) as eng:
+        eng.set_problem(p)
+        if tune:
+            eng.tune(tune)
+        eng.set_overlap(False)
+        eng.run()
+        f0, d0 = eng.forces().copy(), eng.dedr()
+        eng.set_overlap(True)
+        for _ in range(3):
+            eng.run()
+            assert np.array_equal(eng.forces(), f0) and np.array_equal(eng.dedr(), d0)
+    ref = port.run(p, want=("forces",))
+    assert np.abs(f0 - ref["forces"]).max() <= 1e-10 * np.abs(ref["forces"]).max()
