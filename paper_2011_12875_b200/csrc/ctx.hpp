@@ -101,6 +101,7 @@ struct snapgpu_ctx {
   snapgpu::YQuadPlan yqplan;     // quad units (2J > 8)
   snapgpu::host::DevBuf<int4> d_qunits;
   snapgpu::host::DevBuf<double> d_qitw;
+  snapgpu::host::DevBuf<double> d_cwq;  // the quad kernel's padded windowed C' (yquad_cw)
   snapgpu::host::DevBuf<int> d_qrw, d_qrows;
   int y_parts = 0;        // compute_Y CTAs per 32-atom tile forced by snapgpu_tune (0 = automatic)
   int y_parts_max = 1;    // the most parts any tile has in the current plan

@@ -861,7 +861,7 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
   constexpr int NF = c_full_off(T + 1);
   constexpr int NP = NF + 2 * kQPad;
   constexpr int L = MID ? J / 2 + 1 : J + 1;
-  constexpr int JW = J + 1;
+  constexpr int JW = (J + 2) & ~1;  // padded C' row: coefficient pairs in 16-byte loads
   constexpr int U = SNAP_QU;
   const int q = lane >> 3, a = lane & 7;
   double ar[L], ai[L];
@@ -894,10 +894,11 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
 #pragma unroll
       for (int s = 0; s < U; ++s) {
         const double x2r = wt * p2[(a2 + s) * 8], x2i = wt * p2[(NP + a2 + s) * 8];
-        const double* c = c0 + (a2 + s) * JW;
+        const double2* c = reinterpret_cast<const double2*>(c0 + (a2 + s) * JW);
 #pragma unroll
         for (int ma = 0; ma < L; ++ma) {
-          const double cc = __ldg(c + ma);
+          const double2 cp = __ldg(c + (ma >> 1));
+          const double cc = (ma & 1) ? cp.y : cp.x;
           const double wr = er[U - 1 + ma - s], wi = ei[U - 1 + ma - s];
           const double pr = fma(-wi, x2i, wr * x2r);
           const double pi = fma(wi, x2r, wr * x2i);
@@ -915,10 +916,11 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
     }
     for (; a2 <= J2; ++a2) {
       const double x2r = wt * p2[a2 * 8], x2i = wt * p2[(NP + a2) * 8];
-      const double* c = c0 + a2 * JW;
+      const double2* c = reinterpret_cast<const double2*>(c0 + a2 * JW);
 #pragma unroll
       for (int ma = 0; ma < L; ++ma) {
-        const double cc = __ldg(c + ma);
+        const double2 cp = __ldg(c + (ma >> 1));
+        const double cc = (ma & 1) ? cp.y : cp.x;
         const double pr = fma(-ei[U - 1 + ma], x2i, er[U - 1 + ma] * x2r);
         const double pi = fma(ei[U - 1 + ma], x2r, er[U - 1 + ma] * x2i);
         ar[ma] = fma(cc, pr, ar[ma]);

@@ -130,7 +130,7 @@ void launch_Y_t(snapgpu_ctx* c) {
   a.units = c->d_qunits.p;
   a.itw = c->d_qitw.p;
   a.rw = c->d_qrw.p;
-  a.cw = c->d_cw.p;
+  a.cw = c->d_cwq.p;
   a.rows = c->d_qrows.p;
   a.rows_cap = c->yqplan.rows_cap;
   a.nlocal = c->nlocal;

@@ -869,7 +869,8 @@ int snapgpu_create(int device, int twojmax, double rcut, double rmin0, double rf
       build_ycoop(c);
     } else {
       // quad-unit compute_Y: C' and the beta-independent unit tables in HBM
-      up(c->d_cw, c->yplan.cw);
+      up(c->d_cw, c->yplan.cw);  // (the descriptor kernel's layout)
+      up(c->d_cwq, yquad_cw(c->maps, c->yplan.cw));
       c->yqplan = yquad_plan(c->maps, kQWarps / kQGroups, kQGroups);
       std::vector<int4> u(c->yqplan.units.size());
       for (size_t q = 0; q < u.size(); ++q)
@@ -905,6 +906,7 @@ int snapgpu_destroy(snapgpu_ctx* c) {
   c->d_yunits.release();
   c->d_qunits.release();
   c->d_qitw.release();
+  c->d_cwq.release();
   c->d_qrw.release();
   c->d_qrows.release();
   c->d_nlpos.release();

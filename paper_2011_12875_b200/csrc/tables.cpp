@@ -387,11 +387,13 @@ YCoopPlan ycoop_pair_plan(const IndexMaps& m, int warps) {
 
 YQuadPlan yquad_plan(const IndexMaps& m, int warps, int groups) {
   YQuadPlan p;
+  // offsets into the windowed C' with rows padded to even length
+  // (yquad_cw: 16-byte coefficient pairs)
   std::vector<int> cwoff(m.tuples.size());
   int o = 0;
   for (std::size_t q = 0; q < m.tuples.size(); ++q) {
     cwoff[q] = o;
-    o += (m.tuples[q].j2 + 1) * (m.tuples[q].j + 1);
+    o += (m.tuples[q].j2 + 1) * ((m.tuples[q].j + 2) & ~1);
   }
   std::vector<std::pair<double, int>> rowcost;
   for (int j = 0; j <= m.T; ++j)
@@ -444,6 +446,17 @@ YQuadPlan yquad_plan(const IndexMaps& m, int warps, int groups) {
   for (int g = 0; g < groups; ++g)
     for (std::size_t q = 0; q < gb[g].size(); ++q) p.rows[g * p.rows_cap + q] = gb[g][q];
   return p;
+}
+
+std::vector<double> yquad_cw(const IndexMaps& m, const std::vector<double>& cw) {
+  std::vector<double> out;
+  std::size_t src = 0;
+  for (const Tuple& tp : m.tuples)
+    for (int a2 = 0; a2 <= tp.j2; ++a2) {
+      for (int ma = 0; ma < ((tp.j + 2) & ~1); ++ma) out.push_back(ma <= tp.j ? cw[src + ma] : 0.0);
+      src += tp.j + 1;
+    }
+  return out;
 }
 
 std::vector<double> yquad_weights(const YQuadPlan& p, const IndexMaps& m,

@@ -118,6 +118,9 @@ struct YQuadPlan {
   int rows_cap = 0;
 };
 YQuadPlan yquad_plan(const IndexMaps& m, int warps, int groups);
+// y_plan's windowed C' with every row padded to even length (the quad
+// kernel loads coefficient pairs)
+std::vector<double> yquad_cw(const IndexMaps& m, const std::vector<double>& cw);
 std::vector<double> yquad_weights(const YQuadPlan& p, const IndexMaps& m,
                                   const std::vector<double>& wtab);
 
