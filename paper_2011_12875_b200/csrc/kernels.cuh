@@ -1545,13 +1545,37 @@ struct DERCfg {
   static constexpr int NC = T + 1;
   static constexpr int NH = c_half_off(T + 1);
   static constexpr int NIN = T * (T + 1) / 2 > 0 ? T * (T + 1) / 2 : 1;  // inputs of row 0
+  // complex level inputs row r saves (levels max(2r,1)..T; 0 if it never exists)
+  static __host__ __device__ constexpr int nin_row(int r) {
+    return 2 * r > T ? 0 : (T * (T + 1) - (2 * r > 1 ? 2 * r : 1) * ((2 * r > 1 ? 2 * r : 1) - 1)) / 2;
+  }
+  // doubles before row r's block; each block starts on the bank offset
+  // r*PPW (mod 16 doubles), so the warp's 32 lanes (G rows of PPW
+  // consecutive doubles) take the minimum two shared-memory wavefronts
+  static __host__ __device__ constexpr int row_base(int r) {
+    int o = 0;
+    for (int q = 0; q <= r; ++q) {
+      const int want = (q * PPW) % 16;
+      o += ((want - o % 16) + 16) % 16;  // pad to the row's bank offset
+      if (q < r) o += 2 * PPW * nin_row(q);
+    }
+    return o;
+  }
+  // A warp's saved inputs: lane-major [elem][re|im][lane] (every lane
+  // reserves row 0's NIN), or -- where that would cap the warps per SM below
+  // the register bound (2J >= 11: 252 registers, 8 warps) -- packed by row,
+  // [row][elem][re|im][pair of the warp] (2J=12: dE 0.80 -> 0.58 ms, 2J=14:
+  // 3.81 -> 3.61 ms; at 2J <= 10 the lane-major layout is faster).
+  static constexpr bool PACK = NIN * 2 * 32 * 8 * (T <= 8 ? 12 : 8) > 228 * 1024;
+  static constexpr int STRIDE = PACK ? PPW : 32;
+  static constexpr int WSZ = PACK ? (row_base(G) > 0 ? row_base(G) : 2 * PPW) : NIN * 2 * 32;
 #ifndef SNAP_DE_WARPS
   // 2J <= 8: one-warp CTAs, 12 per SM (262k atoms: dE 3.79 -> 3.73 ms)
-  static constexpr int WARPS = T <= 8 ? 1 : (NIN * 2 * 32 * 8 * 4 <= 80 * 1024) ? 4 : 2;
+  static constexpr int WARPS = T <= 8 ? 1 : (WSZ * 8 * 4 <= 80 * 1024) ? 4 : 2;
 #else
   static constexpr int WARPS = SNAP_DE_WARPS;
 #endif
-  static constexpr int SMEM = WARPS * NIN * 2 * 32 * 8;
+  static constexpr int SMEM = WARPS * WSZ * 8;
   // CTAs per SM: 12 warps (register bound) at 2J <= 8
   static constexpr int MINB = T <= 8 ? 12 / WARPS : 1;
 };
@@ -1597,7 +1621,8 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(Y2) + 128 * m));
   PairGeo g;
   pair_geometry<true>(x, y, z, wt, A.gp, g);
-  double* buf = sbuf + (size_t)w * C::NIN * 2 * 32 + lane;  // [elem][re|im][lane]
+  // this lane's inputs: [elem][re|im] with stride PPW inside its row's block
+  double* buf = sbuf + (size_t)w * C::WSZ + (C::PACK ? C::row_base(r) + q : lane);
   const int s0 = (2 * r > 1) ? 2 * r : 1;                    // first level whose input row r stores
   auto in_off = [&](int t) { return (t * (t - 1) - s0 * (s0 - 1)) / 2; };
   const double ar = g.ar, ai = g.ai, br = g.br, bi = g.bi;
@@ -1631,8 +1656,8 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
       const int o = in_off(t);
 #pragma unroll
       for (int c = 0; c < t; ++c) {
-        buf[(size_t)(2 * (o + c)) * 32] = vr[c];
-        buf[(size_t)(2 * (o + c) + 1) * 32] = vi[c];
+        buf[(size_t)(2 * (o + c)) * C::STRIDE] = vr[c];
+        buf[(size_t)(2 * (o + c) + 1) * C::STRIDE] = vi[c];
       }
       if (t < T) {  // the level-T row is never an input
 #pragma unroll
@@ -1719,8 +1744,8 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
     if (active) {
 #pragma unroll
       for (int c = 0; c < t; ++c) {
-        const double pr = buf[(size_t)(2 * (o + c)) * 32];
-        const double pi = buf[(size_t)(2 * (o + c) + 1) * 32];
+        const double pr = buf[(size_t)(2 * (o + c)) * C::STRIDE];
+        const double pi = buf[(size_t)(2 * (o + c) + 1) * C::STRIDE];
         // input P(c) feeds element c (coefficient conj a) and c+1 (-conj b)
         const int h = c & 1;
         Gar[h] = fma(li[c], pi, fma(lr[c], pr, Gar[h]));
@@ -1743,8 +1768,8 @@ __global__ void __launch_bounds__(DERCfg<T>::WARPS * 32, DERCfg<T>::MINB)
         const double K = (((c + T / 2) & 1) ? -R : R);
         const double2 yv = __ldca(Y2 + hb + c);
         const double tlr = yv.x, tli = yv.y;
-        const double ur = buf[(size_t)(2 * (o + T - 1 - c)) * 32];
-        const double ui = buf[(size_t)(2 * (o + T - 1 - c) + 1) * 32];
+        const double ur = buf[(size_t)(2 * (o + T - 1 - c)) * C::STRIDE];
+        const double ui = buf[(size_t)(2 * (o + T - 1 - c) + 1) * C::STRIDE];
         const double pr = K * ur, pi = -K * ui;  // pm(c)
         const int h = c & 1;
         Gar[h] = fma(tli, pi, fma(tlr, pr, Gar[h]));
