@@ -250,6 +250,7 @@ class SnapEngine:
         self.nlocal = 0
         self.stride = 0
         self._keep = ()
+        self._args = {}  # per-argument (object, array, pointer) of the last step call
 
     @classmethod
     def for_problem(cls, p, device=0) -> "SnapEngine":
@@ -344,6 +345,21 @@ class SnapEngine:
     def run(self):
         self._c(self._L.snapgpu_run(self._h))
 
+    def _arg(self, slot, a, dtype):
+        """(array, data pointer) of a step argument.  An argument that is
+        already a C-contiguous `dtype` array is passed as it is, and the same
+        object passed again (an MD loop reusing its pinned buffers) skips the
+        conversion and the pointer lookup: the slot holds a reference, so the
+        buffer cannot move.  Converted copies are never reused (the caller may
+        change the source between calls)."""
+        c = self._args.get(slot)
+        if c is not None and c[0] is a:
+            return c[1], c[2]
+        arr = np.ascontiguousarray(a, dtype)
+        ptr = arr.ctypes.data
+        self._args[slot] = (a, arr, ptr) if arr is a else None
+        return arr, ptr
+
     def step(self, numneigh, nbr, disp, types=None, forces=None, eatom=None, etotal=None,
              natoms_total=None, atom_lo=0, readback=True):
         """One end-to-end force step from host arrays (snapgpu_run_host): upload,
@@ -351,26 +367,26 @@ class SnapEngine:
         arrays when provided.  Returns (forces, eatom, etotal).  With
         readback=False nothing is read back (the results stay on the device,
         e.g. for the partitioned step's reduce-scatter) and None is returned."""
-        nn = np.ascontiguousarray(numneigh, np.int32)
-        nb = np.ascontiguousarray(nbr, np.int32)
-        dp = np.ascontiguousarray(disp, np.float64)
-        ty = None if types is None else np.ascontiguousarray(types, np.int32)
+        nn, pn = self._arg(0, numneigh, np.int32)
+        nb, pb = self._arg(1, nbr, np.int32)
+        dp, pd = self._arg(2, disp, np.float64)
+        ty, pt = (None, None) if types is None else self._arg(3, types, np.int32)
         n = int(nn.shape[0])
         stride = int(nb.shape[1]) if nb.ndim == 2 else int(nb.size // max(n, 1))
         ntot = n if natoms_total is None else int(natoms_total)
         if not readback:
             self._c(self._L.snapgpu_run_host(self._h, ntot, int(atom_lo), n, stride,
-                                             nn.ctypes.data, nb.ctypes.data, dp.ctypes.data,
-                                             _ptr(ty), None, None, None))
+                                             pn, pb, pd, pt, None, None, None))
             self.natoms_total, self.nlocal, self.stride = ntot, n, stride
             self._keep = (nn, nb, dp, ty)
             return None
-        f = forces if forces is not None else np.zeros((ntot, 3), np.float64)
-        e = eatom if eatom is not None else np.zeros(n, np.float64)
-        t = etotal if etotal is not None else np.zeros(1, np.float64)
-        self._c(self._L.snapgpu_run_host(self._h, ntot, int(atom_lo), n, stride, nn.ctypes.data,
-                                         nb.ctypes.data, dp.ctypes.data, _ptr(ty),
-                                         f.ctypes.data, e.ctypes.data, t.ctypes.data))
+        f, pf = self._arg(4, forces if forces is not None else np.zeros((ntot, 3), np.float64),
+                          np.float64)
+        e, pe = self._arg(5, eatom if eatom is not None else np.zeros(n, np.float64), np.float64)
+        t, ptt = self._arg(6, etotal if etotal is not None else np.zeros(1, np.float64),
+                           np.float64)
+        self._c(self._L.snapgpu_run_host(self._h, ntot, int(atom_lo), n, stride, pn, pb, pd, pt,
+                                         pf, pe, ptt))
         self.natoms_total, self.nlocal, self.stride = ntot, n, stride
         self._keep = (nn, nb, dp, ty)
         return f, e, float(t[0])
@@ -449,14 +465,21 @@ class SnapEngine:
         one graph uploads them, rebuilds the neighbor lists on the device,
         runs the force step and reads the results back.  Returns
         (forces, eatom, etotal)."""
-        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
-        n = int(pos.shape[0])
-        bx = np.ascontiguousarray(np.broadcast_to(np.asarray(box, np.float64), (3,)))
-        f = forces if forces is not None else np.zeros((n, 3), np.float64)
-        e = eatom if eatom is not None else np.zeros(n, np.float64)
-        t = etotal if etotal is not None else np.zeros(1, np.float64)
-        self._c(self._L.snapgpu_run_positions(self._h, n, pos.ctypes.data, bx.ctypes.data,
-                                              f.ctypes.data, e.ctypes.data, t.ctypes.data))
+        pos, pp = self._arg(7, positions, np.float64)
+        if pos.size % 3:
+            raise ValueError("positions: expected (natoms, 3) coordinates")
+        n = int(pos.size // 3)
+        if isinstance(box, np.ndarray) and box.shape == (3,):
+            bx, pbx = self._arg(8, box, np.float64)
+        else:
+            bx = np.ascontiguousarray(np.broadcast_to(np.asarray(box, np.float64), (3,)))
+            pbx = bx.ctypes.data
+        f, pf = self._arg(4, forces if forces is not None else np.zeros((n, 3), np.float64),
+                          np.float64)
+        e, pe = self._arg(5, eatom if eatom is not None else np.zeros(n, np.float64), np.float64)
+        t, ptt = self._arg(6, etotal if etotal is not None else np.zeros(1, np.float64),
+                           np.float64)
+        self._c(self._L.snapgpu_run_positions(self._h, n, pp, pbx, pf, pe, ptt))
         self.natoms_total = self.nlocal = n
         return f, e, float(t[0])
 

@@ -58,3 +58,15 @@ pos = pin(p.positions).numpy()
 sp = lambda: eng.step_positions(pos, p.box, forces=f, eatom=e, etotal=t)
 print(f"positions step: {ev_time(sp):.1f} us GPU, {wall(sp):.1f} us wall")
 print(f"graph only wall (sync each): {wall(lambda: (eng.run(), eng.synchronize())):.1f} us")
+# host-side overhead: the Python wrapper's argument handling vs the bare C call
+L, h = eng._L, eng._h
+ptrs = [x.ctypes.data for x in (args[0], args[1], args[2], f, e, t)]
+raw = lambda: L.snapgpu_run_host(h, p.natoms, 0, p.natoms, p.nbr.shape[1], ptrs[0], ptrs[1], ptrs[2],
+                                 None, ptrs[3], ptrs[4], ptrs[5])
+print(f"bare C one-call (precomputed pointers): {wall(raw):.1f} us wall")
+def prep():
+    nn_ = np.ascontiguousarray(args[0], np.int32); nb_ = np.ascontiguousarray(args[1], np.int32)
+    dp_ = np.ascontiguousarray(args[2], np.float64)
+    return (nn_.ctypes.data, nb_.ctypes.data, dp_.ctypes.data, f.ctypes.data, e.ctypes.data, t.ctypes.data)
+print(f"wrapper argument handling only: {wall(prep):.1f} us wall")
+print(f"bare C no-op call (last_error): {wall(lambda: L.snapgpu_last_error(h)):.2f} us wall")

@@ -18,6 +18,36 @@ __global__ void plain(const double* __restrict__ src, double* __restrict__ dst, 
   }
 }
 
+// U2-prepass pattern: lane idx reads pair idx's three displacement components
+// (24-byte stride across lanes); two iterations, serialized (loop) or with all
+// loads issued first (hoisted)
+template <bool HOIST>
+__global__ void aos3(const double* __restrict__ src, double* __restrict__ dst, int per_warp) {
+  const int w = blockIdx.x, lane = threadIdx.x;
+  const int np = per_warp / 3;
+  const double* s = src + (size_t)w * per_warp;
+  double* d = dst + (size_t)w * per_warp;
+  if (HOIST) {
+    double v[2][3];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = lane + 32 * q;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[q][c] = idx < np ? s[idx * 3 + c] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = lane + 32 * q;
+      if (idx < np) d[idx] = v[q][0] + v[q][1] * v[q][2];
+    }
+  } else {
+    for (int idx = lane; idx < np; idx += 32) {
+      const double a = s[idx * 3], b = s[idx * 3 + 1], c = s[idx * 3 + 2];
+      d[idx] = a + b * c;
+    }
+  }
+}
+
 __global__ void bulk(const double* __restrict__ src, double* __restrict__ dst, int per_warp) {
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) unsigned long long mbar;
@@ -55,25 +85,32 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   for (int rep = 0; rep < 3; ++rep) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 4; ++k) {
       for (int it = 0; it < 3; ++it) {
         if (k == 0) plain<<<warps, 32>>>(hd, d, per_warp);
-        else bulk<<<warps, 32, per_warp * 8>>>(hd, d, per_warp);
+        else if (k == 1) bulk<<<warps, 32, per_warp * 8>>>(hd, d, per_warp);
+        else if (k == 2) aos3<false><<<warps, 32>>>(hd, d, 156);
+        else aos3<true><<<warps, 32>>>(hd, d, 156);
       }
       cudaEventRecord(a);
       for (int it = 0; it < 20; ++it) {
         if (k == 0) plain<<<warps, 32>>>(hd, d, per_warp);
-        else bulk<<<warps, 32, per_warp * 8>>>(hd, d, per_warp);
+        else if (k == 1) bulk<<<warps, 32, per_warp * 8>>>(hd, d, per_warp);
+        else if (k == 2) aos3<false><<<warps, 32>>>(hd, d, 156);
+        else aos3<true><<<warps, 32>>>(hd, d, 156);
       }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       double us = ms * 1e3 / 20;
-      printf("%s: %.1f us per %.2f MB -> %.1f GB/s (%s)\n", k ? "bulk " : "plain", us, n * 8 / 1e6,
-             n * 8 / (us * 1e-6) / 1e9, cudaGetErrorString(cudaGetLastError()));
+      const char* nm[4] = {"plain", "bulk ", "aos3 loop", "aos3 hoisted"};
+      const double bytes = k < 2 ? n * 8.0 : warps * 156 * 8.0;
+      printf("%s: %.1f us per %.2f MB -> %.1f GB/s (%s)\n", nm[k], us, bytes / 1e6,
+             bytes / (us * 1e-6) / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
   }
+  plain<<<warps, 32>>>(hd, d, per_warp);  // the check reads the plain copy
   double chk = 0;
   cudaMemcpy(h, d, 8 * 16, cudaMemcpyDeviceToHost);
   for (int i = 0; i < 16; ++i) chk += h[i];
