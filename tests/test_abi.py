@@ -130,3 +130,29 @@ def test_y_launch_plan_covers_every_row_once(ntiles):
     # a forced part count (snapgpu_tune) is uniform
     cta2, _ = _y_plan(T, ntiles, nsm, parts=2)
     assert set(cta2[:, 1] >> 8) == {2} and len(cta2) == 2 * ntiles
+
+
+def test_step_argument_reuse():
+    """SnapEngine._arg: an argument that is already a C-contiguous array of the
+    wanted type is passed as it is and its pointer is reused when the same
+    object comes back; converted copies are rebuilt every call (the source may
+    have changed)."""
+    class _E:
+        _args = {}
+    e = _E()
+    arg = snap.SnapEngine._arg.__get__(e)
+    a = np.zeros((5, 3), np.float64)
+    x, p = arg(0, a, np.float64)
+    assert x is a and p == a.ctypes.data
+    a[0, 0] = 7.0  # in-place changes stay visible through the same buffer
+    x2, p2 = arg(0, a, np.float64)
+    assert x2 is a and p2 == p and x2[0, 0] == 7.0
+    b = np.zeros(4, np.float32)  # converted: never reused
+    y, _ = arg(1, b, np.float64)
+    assert y is not b and y.dtype == np.float64 and e._args[1] is None
+    b[0] = 3.0
+    y2, _ = arg(1, b, np.float64)
+    assert y2[0] == 3.0
+    c = np.zeros((4, 6))[:, ::2]  # non-contiguous: converted
+    z, _ = arg(2, c, np.float64)
+    assert z.flags.c_contiguous and z is not c
