@@ -1,3 +1,3 @@
-for b in _build _build_nl8 _build_nl12; do
-ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -k regex:k_nl_lists -s 2 -c 6 --csv python tools/pos_probe.py --lib=paper_2011_12875_b200/$b/libsnapgpu.so 8 2>/dev/null > gpurun_out/pos_warm_$b.csv
-done
+bash tools/ab_time.sh _build_head _build
+python tools/e2e_parts.py > gpurun_out/e2e_parts22.log 2>&1
+python -m pytest tests/test_gpu_determinism.py tests/test_gpu_parity.py -q -x > gpurun_out/par2.log 2>&1
