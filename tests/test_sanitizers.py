@@ -22,6 +22,12 @@ def test_compute_sanitizer(tool):
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not installed")
+    if "/graft/" in os.path.realpath(cs):
+        # the GPU pool wraps compute-sanitizer and keeps it closed (runs under
+        # it have left GPUs needing a reset); the pool's policy is honoured,
+        # not bypassed through the CUDA toolkit's own binary.  The round-2
+        # runs made before it closed are in profiles/r02_sanitizers.txt.
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     cmd = [cs, "--tool", tool, "--error-exitcode", "9"]
     if tool == "memcheck":
         cmd += ["--leak-check", "full"]
@@ -40,6 +46,8 @@ def test_compute_sanitizer(tool):
             if attempt == 1:
                 pytest.fail(f"{tool} timed out twice; last output:\n{(stdout + stderr)[-2000:]}")
     tail = (stdout + stderr)[-4000:]
+    if proc.returncode == 86 and "closed on this pool" in tail:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert proc.returncode == 0, tail
     assert "sanitize_step: done" in stdout, tail
     text = stdout + stderr
