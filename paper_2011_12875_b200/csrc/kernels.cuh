@@ -823,8 +823,20 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
 // and their partial rows are combined by two xor-shuffles.  12 warps share
 // each target row (LPT over units), partial rows meet in shared memory.
 // ===========================================================================
+// item-pair lanes (yq_row) at 2J >= 11; one item per lane at 2J = 9, 10
+// (2J = 10: 1.23 ms item lanes vs 1.26 ms pairs, 8192 atoms)
+#ifndef SNAP_QPAIR
+#if defined(SNAP_T) && SNAP_T >= 11
+#define SNAP_QPAIR 1
+#else
+#define SNAP_QPAIR 0
+#endif
+#endif
+// window block length.  Item lanes: 2J=14 U = 2 / 3 -> 32.1 / 31.4 ms; 2J=12
+// U = 1 / 2 / 3 -> 7.07 / 6.56 / 6.43 ms (older kernel).  Item pairs: U = 3 /
+// 4 -> 29.3 / 28.9 ms at 2J=14 (32768 atoms), 3.19 / 3.17 ms at 2J=12.
 #ifndef SNAP_QU
-#define SNAP_QU 3  // window block length (2J=14: U = 2 / 3 -> 32.1 / 31.4 ms; 2J=12: U = 1 / 2 / 3 -> 7.07 / 6.56 / 6.43 ms)
+#define SNAP_QU (SNAP_QPAIR ? 4 : 3)
 #endif
 constexpr int kQPad = 16;  // X pad: window reads reach J2+1 <= 15 below, D <= 14 above
 constexpr int kQWarps = 12;
@@ -864,6 +876,141 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
   constexpr int JW = (J + 2) & ~1;  // padded C' row: coefficient pairs in 16-byte loads
   constexpr int U = SNAP_QU;
   const int q = lane >> 3, a = lane & 7;
+#if SNAP_QPAIR
+  // lane = (item pair h = lane/16, output half m = lane/8 % 2, atom a): the
+  // lane runs items 2h and 2h+1 of the unit (same tuple and target row, hence
+  // the same C' at every step) and the outputs ma = m L0 .. m L0 + L0 - 1, so
+  // the two items' complex products are summed before the one C' multiply
+  // (10 FP64 instructions per two items instead of 12).  Outputs past L (odd
+  // L, m = 1) read finite neighbours and are dropped.
+  constexpr int L0 = (L + 1) / 2;
+  const int h = lane >> 4, mo = ((lane >> 3) & 1) * L0;
+  double ar[L0], ai[L0];
+#pragma unroll
+  for (int m = 0; m < L0; ++m) ar[m] = ai[m] = 0.0;
+  const int b = __ldg(A.rw + rid * (NW + 1) + w), e = __ldg(A.rw + rid * (NW + 1) + w + 1);
+  for (int it = b; it < e; ++it) {
+    const int4 u = __ldg(A.units + it);
+    const int J2 = u.y & 0xff, J1 = (u.y >> 8) & 0xff, cnt = u.y >> 16;
+    const double* p1[2];
+    const double* p2[2];
+    double wt[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int i = 2 * h + t;
+      const bool act = i < cnt;
+      const int x1 = act ? (u.x & 0xffff) + i * (J1 + 1) : 0;
+      const int x2 = act ? (u.x >> 16) - i * (J2 + 1) : 0;
+      wt[t] = act ? __ldg(A.itw + u.w + i) : 0.0;
+      p1[t] = sX + (kQPad + x1 + mo) * 8 + a;  // x1[base + mo + k] at p1[k*8]
+      p2[t] = sX + (kQPad + x2) * 8 + a;
+    }
+    const double* c0 = A.cw + u.z + mo;
+    // register window: x1[mo + ma - a2 - s] of both items, shifted by U
+    // every block (reading it straight from shared memory every block was
+    // measured slower: 2J=14 Y 28.9 -> 31.4 ms)
+    double er[2][L0 + U - 1], ei[2][L0 + U - 1];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int ma = 0; ma < L0; ++ma) {
+        er[t][U - 1 + ma] = p1[t][ma * 8];
+        ei[t][U - 1 + ma] = p1[t][(NP + ma) * 8];
+      }
+    int a2 = 0;
+    for (; a2 + U - 1 <= J2; a2 += U) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int k = 1; k < U; ++k) {
+          er[t][U - 1 - k] = p1[t][(-a2 - k) * 8];
+          ei[t][U - 1 - k] = p1[t][(NP - a2 - k) * 8];
+        }
+#pragma unroll
+      for (int s = 0; s < U; ++s) {
+        double x2r[2], x2i[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          x2r[t] = wt[t] * p2[t][(a2 + s) * 8];
+          x2i[t] = wt[t] * p2[t][(NP + a2 + s) * 8];
+        }
+        const double* c = c0 + (a2 + s) * JW;
+#pragma unroll
+        for (int ma = 0; ma < L0; ++ma) {
+          const double cc = __ldg(c + ma);
+          double pr = er[0][U - 1 + ma - s] * x2r[0];
+          double pi = er[0][U - 1 + ma - s] * x2i[0];
+          pr = fma(-ei[0][U - 1 + ma - s], x2i[0], pr);
+          pi = fma(ei[0][U - 1 + ma - s], x2r[0], pi);
+          pr = fma(er[1][U - 1 + ma - s], x2r[1], pr);
+          pi = fma(er[1][U - 1 + ma - s], x2i[1], pi);
+          pr = fma(-ei[1][U - 1 + ma - s], x2i[1], pr);
+          pi = fma(ei[1][U - 1 + ma - s], x2r[1], pi);
+          ar[ma] = fma(cc, pr, ar[ma]);
+          ai[ma] = fma(cc, pi, ai[ma]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+#pragma unroll
+        for (int ma = L0 - 1; ma >= 1; --ma) {
+          er[t][U - 1 + ma] = er[t][ma - 1];
+          ei[t][U - 1 + ma] = ei[t][ma - 1];
+        }
+        er[t][U - 1] = p1[t][(-a2 - U) * 8];
+        ei[t][U - 1] = p1[t][(NP - a2 - U) * 8];
+      }
+    }
+    for (; a2 <= J2; ++a2) {
+      double x2r[2], x2i[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        x2r[t] = wt[t] * p2[t][a2 * 8];
+        x2i[t] = wt[t] * p2[t][(NP + a2) * 8];
+      }
+      const double* c = c0 + a2 * JW;
+#pragma unroll
+      for (int ma = 0; ma < L0; ++ma) {
+        const double cc = __ldg(c + ma);
+        double pr = er[0][U - 1 + ma] * x2r[0];
+        double pi = er[0][U - 1 + ma] * x2i[0];
+        pr = fma(-ei[0][U - 1 + ma], x2i[0], pr);
+        pi = fma(ei[0][U - 1 + ma], x2r[0], pi);
+        pr = fma(er[1][U - 1 + ma], x2r[1], pr);
+        pi = fma(er[1][U - 1 + ma], x2i[1], pi);
+        pr = fma(-ei[1][U - 1 + ma], x2i[1], pr);
+        pi = fma(ei[1][U - 1 + ma], x2r[1], pi);
+        ar[ma] = fma(cc, pr, ar[ma]);
+        ai[ma] = fma(cc, pi, ai[ma]);
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+#pragma unroll
+        for (int ma = L0 - 1; ma > 0; --ma) {
+          er[t][U - 1 + ma] = er[t][U - 2 + ma];
+          ei[t][U - 1 + ma] = ei[t][U - 2 + ma];
+        }
+        er[t][U - 1] = p1[t][(-a2 - 1) * 8];
+        ei[t][U - 1] = p1[t][(NP - a2 - 1) * 8];
+      }
+    }
+  }
+  // combine the two item pairs, partial rows -> shared
+#pragma unroll
+  for (int m = 0; m < L0; ++m) {
+    ar[m] += __shfl_xor_sync(0xffffffffu, ar[m], 16);
+    ai[m] += __shfl_xor_sync(0xffffffffu, ai[m], 16);
+  }
+  if (h == 0) {
+#pragma unroll
+    for (int m = 0; m < L0; ++m) {
+      if (mo + m < L) {
+        sred[((w * (T + 1) + mo + m) * 2 + 0) * 8 + a] = ar[m];
+        sred[((w * (T + 1) + mo + m) * 2 + 1) * 8 + a] = ai[m];
+      }
+    }
+  }
+#else
   double ar[L], ai[L];
 #pragma unroll
   for (int m = 0; m < L; ++m) ar[m] = ai[m] = 0.0;
@@ -950,6 +1097,7 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
       sred[((w * (T + 1) + m) * 2 + 1) * 8 + a] = ai[m];
     }
   }
+#endif
   yq_sync(g, NW * 32);
   constexpr int NH = c_half_off(T + 1);
   const int hb = c_half_off(J) + mb * (J + 1);
