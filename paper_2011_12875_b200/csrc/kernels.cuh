@@ -1314,7 +1314,10 @@ constexpr int kMaxYParts = 8;         // CTAs per tile (row split) at most
 // over several CTAs: 2000 atoms, Y 81.9 -> 75.8 us).  The row-pair units of
 // every target row are LPT-split over the group's warps, sorted by tuple
 // within a warp so the warps of a group sweep the C' table together.
-constexpr int kYGroupWarps = 4;
+#ifndef SNAP_Y_GROUP_WARPS
+#define SNAP_Y_GROUP_WARPS 4
+#endif
+constexpr int kYGroupWarps = SNAP_Y_GROUP_WARPS;
 constexpr int kYGroups = kYWarps / kYGroupWarps;
 static_assert(kYGroups * kYGroupWarps == kYWarps, "whole warp groups");
 // partial-row slots: warp 0 of a group keeps its partial row in registers and
