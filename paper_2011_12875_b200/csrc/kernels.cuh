@@ -840,7 +840,10 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
 #endif
 constexpr int kQPad = 16;  // X pad: window reads reach J2+1 <= 15 below, D <= 14 above
 constexpr int kQWarps = 12;
-constexpr int kQGroups = 3;  // independent warp groups per quad-unit CTA
+#ifndef SNAP_Q_GROUPS
+#define SNAP_Q_GROUPS 3
+#endif
+constexpr int kQGroups = SNAP_Q_GROUPS;  // independent warp groups per quad-unit CTA
 
 struct YQArgs {
   const double* V;
