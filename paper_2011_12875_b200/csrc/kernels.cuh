@@ -820,8 +820,10 @@ __device__ __forceinline__ void energy_epilogue(const EnergyOut& E, double lane_
 // (item slot q = lane/8, atom a = lane%8).  A unit is up to 4 items of one
 // (tuple, target row) — consecutive mb1 — so the 4 lane groups run the same
 // loop with the same C' coefficient at every step (one warp-uniform load)
-// and their partial rows are combined by two xor-shuffles.  12 warps share
-// each target row (LPT over units), partial rows meet in shared memory.
+// and their partial rows are combined by two xor-shuffles.  At 2J >= 11 a
+// lane runs an item pair over half the outputs instead (yq_row, SNAP_QPAIR).
+// 12 warps share each target row (LPT over units), partial rows meet in
+// shared memory.
 // ===========================================================================
 // item-pair lanes (yq_row) at 2J >= 11; one item per lane at 2J = 9, 10
 // (2J = 10: 1.23 ms item lanes vs 1.26 ms pairs, 8192 atoms)
