@@ -29,6 +29,9 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef SNAP_BOUNDS_CHECK
+#include <assert.h>
+#endif
 
 namespace snapgpu {
 
@@ -911,6 +914,18 @@ __device__ __forceinline__ void yq_row(const double* __restrict__ sX, double* __
       p2[t] = sX + (kQPad + x2) * 8 + a;
     }
     const double* c0 = A.cw + u.z + mo;
+#ifdef SNAP_BOUNDS_CHECK  // development build (compute-sanitizer is unavailable on the pool)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int i = 2 * h + t;
+      const int x1 = i < cnt ? (u.x & 0xffff) + i * (J1 + 1) : 0;
+      const int x2 = i < cnt ? (u.x >> 16) - i * (J2 + 1) : 0;
+      // x1 window reads: offsets -(J2 + 1) .. L0 - 1 around x1 + mo; x2: 0 .. J2
+      assert(kQPad + x1 + mo - (J2 + 1) >= 0 && kQPad + x1 + mo + L0 - 1 < NP);
+      assert(kQPad + x2 >= 0 && kQPad + x2 + J2 < NP);
+    }
+    assert(mo + L0 - 1 < JW);  // C' reads stay inside the padded row
+#endif
     // register window: x1[mo + ma - a2 - s] of both items, shifted by U
     // every block (reading it straight from shared memory every block was
     // measured slower: 2J=14 Y 28.9 -> 31.4 ms)
